@@ -1,0 +1,218 @@
+/*
+ * relserve.h -- C ABI of the B200-native RelServe scheduling hot path.
+ *
+ * The reference (`relsim`, pure Python) has no FFI; its "operator API" is the
+ * Python call `relsim.engine.run(trace, policy, world_model, config,
+ * policy_model, seed) -> RunResult` (pkg/src/relsim/engine.py:466-475) and the
+ * `Engine(...)` class with the same constructor (engine.py:180-239).  This ABI
+ * is what a binding for that call needs: plain pointers and sizes, no torch
+ * types.  The Python package `paper_2601_11546_b200` binds it with ctypes
+ * (see INTEGRATION.md for the binding a relsim maintainer would add).
+ *
+ * All entry points return an RS_* status code; rs_last_error() returns a
+ * thread-local message for the last failure on the calling thread.
+ */
+#ifndef RELSERVE_H_
+#define RELSERVE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (the Python shim re-raises the matching reference exception) */
+enum {
+  RS_OK = 0,
+  RS_EINVAL = 1,          /* ValueError: bad policy/tau/constraints (engine.py:189-190, priority.py:36-40,250-251) */
+  RS_EINFEASIBLE = 2,     /* InfeasibleRequestError: tok+output_limit > cap (engine.py:235-239) */
+  RS_EABORT_LIMIT = 3,    /* SimulationAborted: iteration limit (engine.py:376-379) */
+  RS_EABORT_IDLE = 4,     /* SimulationAborted: idle with live relQueries, no arrivals (engine.py:441-445) */
+  RS_ECACHE_PINNED = 5,   /* RuntimeError: prefix cache cannot evict (prefix_cache.py:138) */
+  RS_ECUDA = 6,           /* CUDA runtime failure */
+  RS_ENOMEM = 7,
+  RS_EUNSUPPORTED = 8,    /* input outside the device model (e.g. non-forest prefix structure) */
+  RS_RUNNING = 100        /* trace not finished yet (status of a live trace) */
+};
+
+/* ---- policies (engine.py:45) */
+enum {
+  RS_POLICY_FCFS = 0,
+  RS_POLICY_SP = 1,
+  RS_POLICY_RELSERVE = 2,
+  RS_POLICY_RELSERVE_PP = 3,
+  RS_POLICY_RELSERVE_DP = 4
+};
+
+/* ---- decision enums (arranger.py:30-40) */
+enum { RS_ACTION_PREFILL = 0, RS_ACTION_DECODE = 1, RS_ACTION_IDLE = 2 };
+enum { RS_CASE_PREEMPT = 0, RS_CASE_INTERNAL = 1, RS_CASE_TRANSITIONAL = 2, RS_CASE_FORCED = 3 };
+
+/* Iteration cost model alpha*x + beta (cost_model.py:23-58). */
+typedef struct {
+  double alpha_p, beta_p, alpha_d, beta_d;
+} rs_cost_model;
+
+/* EngineConfig (engine.py:141-158) + SchedulerConstraints (priority.py:30-40). */
+typedef struct {
+  int64_t cap;                    /* max resident tokens */
+  int64_t max_num_seqs;           /* mns */
+  int64_t max_num_batched_tokens; /* mnbt */
+  int64_t sample_size;            /* DPU cache-miss sample size */
+  double tau;                     /* starvation threshold (INFINITY disables) */
+  double noise_sigma;             /* world-model noise; only 0 is supported */
+  int64_t block_size;             /* prefix-cache block (tokens) */
+  int64_t capacity_blocks;        /* prefix-cache capacity (blocks) */
+  int64_t iteration_limit;
+  int32_t log_decisions;          /* record one rs_iter_record per iteration */
+  int32_t policy;                 /* RS_POLICY_* */
+} rs_config;
+
+/* numpy PCG64 bit-generator state (`Generator.bit_generator.state`). */
+typedef struct {
+  uint64_t state_hi, state_lo;
+  uint64_t inc_hi, inc_lo;
+  uint32_t has_uint32, uinteger;
+} rs_pcg64_state;
+
+/*
+ * One trace, column-wise, in trace order (the order of ArrivalTrace.entries).
+ * Rows of relQuery i are row_off[i] .. row_off[i+1]-1 in req_id order.
+ * chain_blocks[i] = number of leading whole blocks shared by every row of
+ * relQuery i; all other blocks of a row are private to it (the prefix-cache
+ * forest structure of generate_trace/load_trace traces).
+ * static_prio may be NULL except for RS_POLICY_SP (static_relquery_prio,
+ * priority.py:230-235, evaluated on the host because its mappings are
+ * arbitrary callables in the reference).
+ */
+typedef struct {
+  int64_t num_relqueries;
+  int64_t num_requests;
+  const int64_t* rel_id;        /* [R] */
+  const double* arrival;        /* [R] */
+  const int32_t* output_limit;  /* [R] */
+  const int64_t* row_off;       /* [R+1] */
+  const int32_t* tok;           /* [N] input tokens */
+  const int32_t* out;           /* [N] actual_output_len (simulated EOS) */
+  const int32_t* chain_blocks;  /* [R] */
+  const double* static_prio;    /* [R] or NULL */
+} rs_trace_view;
+
+/*
+ * One scheduler iteration (DecisionLogEntry, engine.py:64-74, plus what the
+ * parity tests compare).  Optional floats are NaN when the reference has None.
+ * relQuery indices are trace-order indices (map through rel_id[]).
+ */
+typedef struct {
+  int64_t iteration;
+  double clock;          /* clock when the decision was taken */
+  double m_plus, m_minus;
+  double delta_plus, delta_minus, delta_total;
+  int64_t kv_reserved;   /* after execution */
+  int32_t action;        /* RS_ACTION_* */
+  int32_t kase;          /* RS_CASE_* */
+  int32_t head;          /* waiting[0] relQuery index, -1 if none */
+  int32_t n_waiting;     /* len(waiting) after the priority update */
+  int32_t batch_rq;      /* prefill: relQuery index; else -1 */
+  int32_t batch_first;   /* prefill: first req_id taken */
+  int32_t batch_n;       /* prefill: rows taken; decode: batch size; idle: 0 */
+  int32_t n_reestimated; /* relQueries whose priority was recomputed */
+} rs_iter_record;
+
+/* Per-trace progress/result summary (RunResult scalars, engine.py:77-102). */
+typedef struct {
+  int64_t iterations;
+  double clock;                /* sim_duration when finished */
+  int64_t cache_hit_tokens;
+  int64_t cache_miss_tokens;
+  int64_t kv_reserved;
+  int64_t n_log;               /* decision records written so far */
+  int64_t live_relqueries;
+  int64_t admitted;
+  int32_t status;              /* RS_RUNNING, RS_OK (finished) or an error code */
+  int32_t error_detail;
+  rs_pcg64_state rng;          /* DPU RNG state */
+} rs_trace_status;
+
+typedef struct rs_engine rs_engine;
+
+/* Last error message on this thread. */
+const char* rs_last_error(void);
+
+/* Library build/device info, e.g. "sm_100a". */
+const char* rs_build_info(void);
+
+/*
+ * Create an engine over n_traces independent traces (one device scheduler
+ * per trace) and upload their state to `device`.  Replaces the Engine
+ * constructor (engine.py:180-239): validates the policy/config, rejects
+ * infeasible requests, and seeds each trace's DPU RNG from rng[t] (numpy
+ * `default_rng(SeedSequence([seed, 0xD9]))`, engine.py:224).
+ * log_capacity = decision records kept per trace between rs_engine_read_log
+ * calls (records beyond it are dropped; status.n_log still counts them).
+ */
+int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_config* cfg,
+                     const rs_cost_model* world, const rs_cost_model* policy_model,
+                     const rs_pcg64_state* rng, int32_t device, int64_t log_capacity,
+                     rs_engine** out);
+
+/*
+ * Advance every unfinished trace by up to max_iters scheduler iterations
+ * (one pass of Engine.run's loop body, engine.py:375-448, each).  Enqueued
+ * on `stream` (a cudaStream_t, NULL = legacy default); does not synchronize.
+ */
+int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream);
+
+/* Synchronize `stream` and copy every trace's status to status[n_traces]. */
+int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* status);
+
+/* Copy decision records [first, first+count) of trace t (must still be in the buffer). */
+int rs_engine_read_log(rs_engine* e, int32_t t, int64_t first, int64_t count, rs_iter_record* out);
+
+/* Timestamp ledgers per relQuery in trace order; NaN = None (engine.py:52-61). */
+int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* first_prefill_start,
+                           double* last_prefill_end, double* last_decode_end);
+
+/*
+ * Per-request final state in trace order: generated tokens, prefilled flag,
+ * completion iteration (-1 = not finished), and the last priority written.
+ * Any pointer may be NULL.
+ */
+int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t* prefilled,
+                            int64_t* completion_iter, double* priority);
+
+/* Release all device memory of the engine. */
+void rs_engine_destroy(rs_engine* e);
+
+/* Device bytes held per trace (SoA + scratch), for reporting. */
+int64_t rs_engine_device_bytes(const rs_engine* e);
+
+/* ---------------------------------------------------------------------------
+ * Unit entry points (parity tests); same device code as the engine.
+ * ------------------------------------------------------------------------- */
+
+/*
+ * pem() (priority.py:163-218) for n_sets remainders on the device.  Items of
+ * set s are item_off[s] .. item_off[s+1]-1 in request order; utok is the
+ * estimator's uncached-token count (0 if prefilled), remaining = decode
+ * iterations left, prefilled in {0,1}.  Host buffers; synchronous.
+ */
+int rs_pem_batch(int64_t n_sets, const int64_t* item_off, const int64_t* utok,
+                 const int32_t* remaining, const uint8_t* prefilled, int64_t cap,
+                 int64_t max_num_seqs, int64_t max_num_batched_tokens,
+                 const rs_cost_model* model, double* values_out, int32_t device);
+
+/*
+ * numpy Generator.choice(n, k, replace=False) replay for a sequence of calls
+ * (prefix_cache.py:157-158): call c draws k[c] of n[c] (k < n, Floyd path),
+ * writing the k[c] indices at idx_out[off] (off = running sum of k).  The
+ * final generator state is written back to *rng.  Host buffers; synchronous.
+ */
+int rs_choice_sequence(rs_pcg64_state* rng, int64_t n_calls, const int64_t* n, const int64_t* k,
+                       int64_t* idx_out, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RELSERVE_H_ */

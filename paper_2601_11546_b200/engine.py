@@ -1,0 +1,333 @@
+"""GPU-resident scheduling engine: drop-in for `relsim.engine` (engine.py:45-475).
+
+`run(trace, policy, world_model, config, policy_model, seed) -> RunResult` and
+`Engine(...)` keep the reference signatures.  Every scheduler iteration --
+admission, the Dynamic Priority Updater with its PEM estimator and numpy
+PCG64 sample replay, the waiting-queue order, the Adaptive Batch Arranger
+with the Delta projection, and the prefill/decode/idle state advance with the
+prefix-cache model -- runs on the GPU inside one persistent sm_100a kernel
+per trace (paper_2601_11546_b200/csrc/engine.cu).  The host only uploads the
+trace columns, launches chunks of iterations and copies back the decision
+records, ledgers and per-request state.  There is no CPU fallback: if the
+CUDA library is missing or the GPU is absent, construction fails.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi, _marshal
+from .cost_model import LinearCostModel
+from .priority import InfeasibleRequestError, SchedulerConstraints
+from .workload import ArrivalTrace
+
+POLICIES = ("fcfs", "sp", "relserve", "relserve-pp", "relserve-dp")
+
+
+class SimulationAborted(RuntimeError):
+    pass
+
+
+@dataclass
+class TimestampLedger:
+    arrival: float
+    first_prefill_start: float | None = None
+    last_prefill_end: float | None = None
+    last_decode_end: float | None = None
+
+    @property
+    def complete(self) -> bool:
+        return self.last_decode_end is not None
+
+
+@dataclass
+class DecisionLogEntry:
+    iteration: int
+    clock: float
+    case: str
+    m_plus: float | None
+    m_minus: float | None
+    delta_plus: float | None
+    delta_minus: float | None
+    delta_total: float | None
+    action: str
+
+
+@dataclass
+class RunResult:
+    """Mirror of relsim's RunResult (engine.py:77-138) plus device-side extras."""
+
+    policy: str
+    rate: float
+    seed: int
+    ledgers: dict[int, TimestampLedger]
+    relquery_sizes: dict[int, int]
+    decision_log: list[DecisionLogEntry]
+    iterations: int
+    sim_duration: float
+    dpu_wall_s: float
+    aba_wall_s: float
+    cache_hit_tokens: int
+    cache_miss_tokens: int
+    #: per request (trace order): iteration of the decode that completed it, -1 if none
+    completion_iteration: np.ndarray | None = None
+    #: raw per-iteration records (include/relserve.h rs_iter_record)
+    records: np.ndarray | None = None
+    #: wall time of the whole device run (host view, includes launches/copies)
+    device_wall_s: float = 0.0
+
+    @property
+    def cache_hit_ratio(self) -> float:
+        total = self.cache_hit_tokens + self.cache_miss_tokens
+        return self.cache_hit_tokens / total if total else 0.0
+
+    @property
+    def scheduler_overhead_fraction(self) -> float:
+        if self.sim_duration <= 0:
+            return 0.0
+        return (self.dpu_wall_s + self.aba_wall_s) / self.sim_duration
+
+    def write_relquery_csv(self, path) -> None:
+        import csv
+        from pathlib import Path
+
+        from .report import decompose
+
+        with Path(path).open("w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["rel_id", "size", "arrival_s", "waiting_s", "core_s", "tail_s", "total_s"])
+            for rel_id in sorted(self.ledgers):
+                led = self.ledgers[rel_id]
+                b = decompose(rel_id, led)
+                w.writerow([rel_id, self.relquery_sizes[rel_id], repr(led.arrival), repr(b.waiting_s),
+                            repr(b.core_s), repr(b.tail_s), repr(b.total_s)])
+
+    def write_decision_csv(self, path) -> None:
+        import csv
+        from pathlib import Path
+
+        with Path(path).open("w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["iteration", "clock_s", "case", "m_plus", "m_minus",
+                        "delta_plus", "delta_minus", "delta_total", "action"])
+            for e in self.decision_log:
+                w.writerow([e.iteration, repr(e.clock), e.case, e.m_plus, e.m_minus,
+                            e.delta_plus, e.delta_minus, e.delta_total, e.action])
+
+
+@dataclass
+class EngineConfig:
+    """Mirror of relsim's EngineConfig (engine.py:141-158)."""
+
+    constraints: SchedulerConstraints = field(
+        default_factory=lambda: SchedulerConstraints(
+            cap=200_000, max_num_seqs=256, max_num_batched_tokens=8192
+        )
+    )
+    noise_sigma: float = 0.0
+    sample_size: int = 8
+    tau: float = math.inf
+    block_size: int = 16
+    capacity_blocks: int = 8192
+    iteration_limit: int = 5_000_000
+    log_decisions: bool = True
+    sp_priority_fns: tuple | None = None
+
+
+def _opt(x: float):
+    return None if math.isnan(x) else float(x)
+
+
+_ERRORS = {
+    _abi.RS_EINVAL: ValueError,
+    _abi.RS_EINFEASIBLE: InfeasibleRequestError,
+    _abi.RS_EABORT_LIMIT: SimulationAborted,
+    _abi.RS_EABORT_IDLE: SimulationAborted,
+    _abi.RS_ECACHE_PINNED: RuntimeError,
+    _abi.RS_EUNSUPPORTED: NotImplementedError,
+}
+
+
+def raise_for(code: int, msg: str):
+    if code in (_abi.RS_OK, _abi.RS_RUNNING):
+        return
+    raise _ERRORS.get(code, RuntimeError)(msg)
+
+
+class Engine:
+    """Reference-signature engine whose loop runs on the GPU (engine.py:179-463)."""
+
+    #: iterations launched per device step (one persistent-kernel launch)
+    chunk_iterations = 1 << 14
+
+    def __init__(
+        self,
+        trace: ArrivalTrace,
+        policy: str,
+        world_model: LinearCostModel,
+        config: EngineConfig | None = None,
+        policy_model: LinearCostModel | None = None,
+        seed: int = 0,
+        *,
+        device: int = 0,
+        stream=None,
+    ):
+        if policy not in POLICIES:
+            raise ValueError(f"unknown policy {policy!r}; choose from {POLICIES}")
+        self.trace = trace
+        self.policy = policy
+        self.world_model = world_model
+        self.policy_model = policy_model if policy_model is not None else world_model
+        self.config = config or EngineConfig()
+        self.seed = seed
+        self.device = device
+        self.stream = stream
+        c = self.config
+        if policy in ("relserve", "relserve-pp", "relserve-dp") and not (c.tau > 0):
+            raise ValueError("tau must be positive")
+        if c.noise_sigma > 0:
+            raise NotImplementedError(
+                "world-model noise (numpy standard_normal replay) is not on the device path yet")
+        from . import _native
+
+        self._m = _marshal.marshal_trace(trace, c.block_size, policy, self.policy_model,
+                                         c.sp_priority_fns)
+        self._native = _native.NativeEngine(
+            [self._m.view], _marshal.make_config(c, policy), _marshal.make_model(world_model),
+            _marshal.make_model(self.policy_model), [_marshal.dpu_rng_state(seed)], device,
+            log_capacity=self.chunk_iterations if c.log_decisions else 0,
+        )
+        self.iteration = 0
+        self.clock = 0.0
+        self.kv_reserved = 0
+        self._records: list[np.ndarray] = []
+        self._status = None
+        self.result: RunResult | None = None
+
+    # -- device loop ---------------------------------------------------------
+
+    def step(self, max_iterations: int) -> _abi.TraceStatus:
+        """Run up to max_iterations scheduler iterations on the device."""
+        ne = self._native
+        ne.step(max_iterations, self.stream)
+        st = ne.status(self.stream)[0]
+        if self.config.log_decisions and st.n_log > self._n_read:
+            self._records.append(ne.read_log(0, self._n_read, st.n_log - self._n_read))
+            self._n_read = st.n_log
+        self._status = st
+        self.iteration = st.iterations
+        self.clock = st.clock
+        self.kv_reserved = st.kv_reserved
+        return st
+
+    _n_read = 0
+
+    def run(self) -> RunResult:
+        t0 = time.perf_counter()
+        while True:
+            st = self.step(self.chunk_iterations)
+            if st.status != _abi.RS_RUNNING:
+                break
+        wall = time.perf_counter() - t0
+        self.result = self._collect(wall)
+        if st.status != _abi.RS_OK:
+            msgs = {
+                _abi.RS_EABORT_LIMIT: f"iteration limit {self.config.iteration_limit} exceeded",
+                _abi.RS_EABORT_IDLE: "engine idle with live relQueries and no future arrivals",
+                _abi.RS_ECACHE_PINNED: "prefix cache cannot evict: all resident blocks pinned",
+            }
+            raise_for(st.status, msgs.get(st.status, f"device engine failed with status {st.status}"))
+        return self.result
+
+    def _collect(self, wall: float) -> RunResult:
+        ne = self._native
+        st = self._status
+        c = self.trace.columns()
+        arrival, fps, lpe, lde = ne.read_ledgers(0, c.num_relqueries)
+        gen, pre, comp, prio = ne.read_requests(0, c.num_requests)
+        order = np.lexsort((c.rel_id, c.arrival))
+        admitted = np.zeros(c.num_relqueries, bool)
+        admitted[order[: st.admitted]] = True
+        ledgers = {}
+        for i in order[: st.admitted].tolist():
+            ledgers[int(c.rel_id[i])] = TimestampLedger(
+                float(arrival[i]), _opt(fps[i]), _opt(lpe[i]), _opt(lde[i]))
+        recs = (np.concatenate(self._records) if self._records
+                else np.zeros(0, _abi.ITER_RECORD_DTYPE))
+        log = []
+        if self.config.log_decisions:
+            for r in recs:
+                proj = not math.isnan(r["delta_plus"])
+                log.append(DecisionLogEntry(
+                    int(r["iteration"]), float(r["clock"]), _abi.CASES[r["kase"]],
+                    _opt(r["m_plus"]), _opt(r["m_minus"]),
+                    float(r["delta_plus"]) if proj else None,
+                    float(r["delta_minus"]) if proj else None,
+                    float(r["delta_total"]) if proj else None,
+                    _abi.ACTIONS[r["action"]]))
+        if self.trace.materialized:
+            k = 0
+            g, p, pr = gen.tolist(), pre.tolist(), prio.tolist()
+            for q in self.trace.entries:
+                for r in q.requests:
+                    r.generated, r.prefilled, r.priority = g[k], bool(p[k]), pr[k]
+                    k += 1
+        self.requests_state = (gen, pre, comp, prio)
+        return RunResult(
+            policy=self.policy, rate=self.trace.rate, seed=self.seed, ledgers=ledgers,
+            relquery_sizes={int(r): int(s) for r, s in zip(c.rel_id.tolist(), np.diff(c.row_off).tolist())},
+            decision_log=log, iterations=int(st.iterations), sim_duration=float(st.clock),
+            dpu_wall_s=0.0, aba_wall_s=0.0, cache_hit_tokens=int(st.cache_hit_tokens),
+            cache_miss_tokens=int(st.cache_miss_tokens), completion_iteration=comp, records=recs,
+            device_wall_s=wall,
+        )
+
+    @property
+    def running(self) -> list:
+        """Requests prefilled and not done (empty once the run finished)."""
+        if self.result is None:
+            return []
+        gen, pre, _, _ = self.requests_state
+        c = self.trace.columns()
+        idx = np.nonzero((pre != 0) & (gen < c.out))[0]
+        return idx.tolist()
+
+    @property
+    def waiting(self) -> list:
+        if self.result is None:
+            return []
+        _, pre, _, _ = self.requests_state
+        c = self.trace.columns()
+        rq = np.repeat(np.arange(c.num_relqueries), np.diff(c.row_off))
+        return sorted(set(rq[pre == 0].tolist()))
+
+    def close(self):
+        if getattr(self, "_native", None) is not None:
+            self._native.close()
+            self._native = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run(
+    trace: ArrivalTrace,
+    policy: str,
+    world_model: LinearCostModel,
+    config: EngineConfig | None = None,
+    policy_model: LinearCostModel | None = None,
+    seed: int = 0,
+) -> RunResult:
+    """Simulate serving the trace under the given policy to completion, on the GPU."""
+    eng = Engine(trace, policy, world_model, config, policy_model, seed)
+    try:
+        return eng.run()
+    finally:
+        eng.close()
