@@ -1,0 +1,171 @@
+"""ctypes binding of the CUDA library (lib/librelserve_b200.so, include/relserve.h).
+
+Loading fails loudly when the library is missing or no CUDA device is visible:
+the scheduler has no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from . import _abi
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "lib" / "librelserve_b200.so"
+
+_lib = None
+
+
+class NativeLibraryMissing(ImportError):
+    pass
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the scheduler hot path)")
+    L = C.CDLL(str(LIB_PATH))
+    L.rs_last_error.restype = C.c_char_p
+    L.rs_build_info.restype = C.c_char_p
+    L.rs_engine_create.restype = C.c_int
+    L.rs_engine_create.argtypes = [C.POINTER(_abi.TraceView), C.c_int32, C.POINTER(_abi.Config),
+                                   C.POINTER(_abi.CostModel), C.POINTER(_abi.CostModel),
+                                   C.POINTER(_abi.Pcg64State), C.c_int32, C.c_int64, C.POINTER(C.c_void_p)]
+    L.rs_engine_step.restype = C.c_int
+    L.rs_engine_step.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+    L.rs_engine_status.restype = C.c_int
+    L.rs_engine_status.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_abi.TraceStatus)]
+    L.rs_engine_read_log.restype = C.c_int
+    L.rs_engine_read_log.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
+    L.rs_engine_read_ledgers.restype = C.c_int
+    L.rs_engine_read_ledgers.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
+    L.rs_engine_read_requests.restype = C.c_int
+    L.rs_engine_read_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
+    L.rs_engine_destroy.restype = None
+    L.rs_engine_destroy.argtypes = [C.c_void_p]
+    L.rs_engine_device_bytes.restype = C.c_int64
+    L.rs_engine_device_bytes.argtypes = [C.c_void_p]
+    L.rs_pem_batch.restype = C.c_int
+    L.rs_pem_batch.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                               C.c_int64, C.c_int64, C.POINTER(_abi.CostModel), C.c_void_p, C.c_int32]
+    L.rs_choice_sequence.restype = C.c_int
+    L.rs_choice_sequence.argtypes = [C.POINTER(_abi.Pcg64State), C.c_int64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int32]
+    _lib = L
+    return L
+
+
+#: every symbol include/relserve.h declares
+EXPORTED_SYMBOLS = (
+    "rs_last_error", "rs_build_info", "rs_engine_create", "rs_engine_step", "rs_engine_status",
+    "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_destroy",
+    "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence",
+)
+
+
+def _check(rc: int):
+    if rc != _abi.RS_OK:
+        from .engine import raise_for
+
+        msg = lib().rs_last_error().decode()
+        raise_for(rc, msg)
+        raise RuntimeError(f"rc={rc}: {msg}")
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):  # torch.cuda.Stream
+        return int(stream.cuda_stream)
+    return int(stream)
+
+
+class NativeEngine:
+    """Owns an rs_engine handle (device SoA for one or more traces)."""
+
+    def __init__(self, views, cfg: _abi.Config, world: _abi.CostModel, pol: _abi.CostModel, rngs,
+                 device: int, log_capacity: int):
+        L = lib()
+        n = len(views)
+        arr_v = (_abi.TraceView * n)(*views)
+        arr_r = (_abi.Pcg64State * n)(*rngs)
+        h = C.c_void_p()
+        self._cfg, self._world, self._pol = cfg, world, pol
+        _check(L.rs_engine_create(arr_v, n, C.byref(cfg), C.byref(world), C.byref(pol), arr_r, device,
+                                  log_capacity, C.byref(h)))
+        self.h = h
+        self.n = n
+        self.log_capacity = log_capacity
+
+    def step(self, max_iters: int, stream=None):
+        _check(lib().rs_engine_step(self.h, int(max_iters), _stream_ptr(stream)))
+
+    def status(self, stream=None) -> list[_abi.TraceStatus]:
+        st = (_abi.TraceStatus * self.n)()
+        _check(lib().rs_engine_status(self.h, _stream_ptr(stream), st))
+        return list(st)
+
+    def read_log(self, t: int, first: int, count: int) -> np.ndarray:
+        out = np.zeros(count, _abi.ITER_RECORD_DTYPE)
+        if count:
+            _check(lib().rs_engine_read_log(self.h, t, first, count, out.ctypes.data))
+        return out
+
+    def read_ledgers(self, t: int, R: int):
+        a, b, c, d = (np.zeros(R, np.float64) for _ in range(4))
+        _check(lib().rs_engine_read_ledgers(self.h, t, a.ctypes.data, b.ctypes.data, c.ctypes.data,
+                                            d.ctypes.data))
+        return a, b, c, d
+
+    def read_requests(self, t: int, N: int):
+        gen = np.zeros(N, np.int32)
+        pre = np.zeros(N, np.uint8)
+        comp = np.zeros(N, np.int64)
+        prio = np.zeros(N, np.float64)
+        _check(lib().rs_engine_read_requests(self.h, t, gen.ctypes.data, pre.ctypes.data,
+                                             comp.ctypes.data, prio.ctypes.data))
+        return gen, pre, comp, prio
+
+    def device_bytes(self) -> int:
+        return int(lib().rs_engine_device_bytes(self.h))
+
+    def close(self):
+        if self.h:
+            lib().rs_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pem_batch(item_off, utok, rem, pre, constraints, model, device=0) -> np.ndarray:
+    n_sets = len(item_off) - 1
+    out = np.zeros(max(n_sets, 0), np.float64)
+    if n_sets <= 0:
+        return out
+    cm = _abi.CostModel(model.alpha_p, model.beta_p, model.alpha_d, model.beta_d)
+    keep = [np.ascontiguousarray(x) for x in (item_off, utok, rem, pre)]
+    _check(lib().rs_pem_batch(n_sets, *(k.ctypes.data for k in keep), constraints.cap,
+                              constraints.max_num_seqs, constraints.max_num_batched_tokens, C.byref(cm),
+                              out.ctypes.data, device))
+    return out
+
+
+def choice_sequence(state: _abi.Pcg64State, ns, ks, device=0) -> np.ndarray:
+    ns = np.ascontiguousarray(ns, np.int64)
+    ks = np.ascontiguousarray(ks, np.int64)
+    out = np.zeros(max(int(ks.sum()), 1), np.int64)
+    _check(lib().rs_choice_sequence(C.byref(state), len(ns), ns.ctypes.data, ks.ctypes.data,
+                                    out.ctypes.data, device))
+    return out[: int(ks.sum())]

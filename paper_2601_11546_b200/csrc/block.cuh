@@ -1,0 +1,141 @@
+// block.cuh -- CTA-wide scan / reduction primitives (warp shuffles + one smem
+// slot per warp).  All threads of the CTA must call them.
+#pragma once
+#include <stdint.h>
+
+namespace rsd {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T o = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    T o = __shfl_xor_sync(kFull, v, d);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+
+// Scratch for block scans of up to 4 lanes of int64.
+struct ScanSmem {
+  long long w[4][kWarps];
+  long long tot[4];
+};
+
+// Inclusive block scan of N int64 values per thread-slot (N <= 4); returns
+// inclusive prefix in v[], block totals in tot[] (visible after return).
+template <int N>
+__device__ __forceinline__ void block_incl_scan(long long (&v)[N], ScanSmem& sm, long long (&tot)[N]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < N; ++c) v[c] = warp_incl_scan(v[c]);
+  if (lane == 31) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) sm.w[c][warp] = v[c];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      long long x = lane < kWarps ? sm.w[c][lane] : 0;
+      x = warp_incl_scan(x);
+      if (lane < kWarps) sm.w[c][lane] = x;
+      if (lane == kWarps - 1) sm.tot[c] = x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    if (warp > 0) v[c] += sm.w[c][warp - 1];
+    tot[c] = sm.tot[c];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ long long block_sum(long long v, ScanSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sm.w[0][warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    long long x = lane < kWarps ? sm.w[0][lane] : 0;
+    x = warp_sum(x);
+    if (lane == 0) sm.tot[0] = x;
+  }
+  __syncthreads();
+  long long r = sm.tot[0];
+  __syncthreads();
+  return r;
+}
+
+// Argmin over (key, idx) pairs: smallest key, ties -> smallest idx.
+struct ArgminSmem {
+  unsigned long long k[kWarps];
+  long long i[kWarps];
+  unsigned long long rk;
+  long long ri;
+};
+
+__device__ __forceinline__ void argmin_merge(unsigned long long& k, long long& i, unsigned long long ok,
+                                             long long oi) {
+  if (ok < k || (ok == k && oi < i)) {
+    k = ok;
+    i = oi;
+  }
+}
+
+__device__ __forceinline__ void block_argmin(unsigned long long& key, long long& idx, ArgminSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    unsigned long long ok = __shfl_xor_sync(kFull, key, d);
+    long long oi = __shfl_xor_sync(kFull, idx, d);
+    argmin_merge(key, idx, ok, oi);
+  }
+  if (lane == 0) {
+    sm.k[warp] = key;
+    sm.i[warp] = idx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long k = lane < kWarps ? sm.k[lane] : ~0ULL;
+    long long i = lane < kWarps ? sm.i[lane] : (long long)0x7FFFFFFFFFFFFFFFLL;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      unsigned long long ok = __shfl_xor_sync(kFull, k, d);
+      long long oi = __shfl_xor_sync(kFull, i, d);
+      argmin_merge(k, i, ok, oi);
+    }
+    if (lane == 0) {
+      sm.rk = k;
+      sm.ri = i;
+    }
+  }
+  __syncthreads();
+  key = sm.rk;
+  idx = sm.ri;
+  __syncthreads();
+}
+
+}  // namespace rsd

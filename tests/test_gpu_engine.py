@@ -1,0 +1,92 @@
+"""Device engine parity: bit-exact against the real reference's golden runs and
+against the CPU oracle on further seeded traces."""
+
+import math
+
+import numpy as np
+import pytest
+
+import parity
+from golden_util import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def run_device(trace, policy, world, cfg, pm, seed):
+    from paper_2601_11546_b200.engine import Engine, SimulationAborted
+
+    eng = Engine(trace, policy, world, cfg, pm, seed, device=0)
+    aborted = None
+    try:
+        res = eng.run()
+    except SimulationAborted as e:
+        aborted = str(e)
+        res = eng.result
+    eng.close()
+    return res, aborted
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_device_matches_reference_golden(name):
+    g = load_golden(name)
+    trace, policy, world, cfg, pm, seed = parity.golden_inputs(g)
+    res, aborted = run_device(trace, policy, world, cfg, pm, seed)
+    assert (aborted is None) == (g["aborted"] is None)
+    parity.compare_records(res.records, g, trace, f"device/{name}")
+    parity.compare_completion(res.completion_iteration, g, trace)
+    led = res.ledgers
+    c = trace.columns()
+    fps = np.array([led[int(r)].first_prefill_start if int(r) in led and led[int(r)].first_prefill_start is not None
+                    else math.nan for r in c.rel_id])
+    lpe = np.array([led[int(r)].last_prefill_end if int(r) in led and led[int(r)].last_prefill_end is not None
+                    else math.nan for r in c.rel_id])
+    lde = np.array([led[int(r)].last_decode_end if int(r) in led and led[int(r)].last_decode_end is not None
+                    else math.nan for r in c.rel_id])
+    parity.compare_ledgers(fps, lpe, lde, g, trace)
+    want = g["result"]
+    assert res.iterations == want["iterations"]
+    assert res.sim_duration == want["sim_duration"]
+    assert res.cache_hit_tokens == want["cache_hit_tokens"]
+    assert res.cache_miss_tokens == want["cache_miss_tokens"]
+    assert len(res.ledgers) == len(g["ledgers"])
+
+
+CASES = [
+    # (trace config, policy, world, engine config kwargs, seed)
+    (dict(num_relqueries=60, size_range=(1, 200), rate=2.0, seed=31), "relserve", "opt-13b-like", {}, 1),
+    (dict(num_relqueries=40, size_range=(50, 300), rate=50.0, seed=32), "relserve", "llama-70b-like",
+     dict(capacity_blocks=300), 2),
+    (dict(num_relqueries=50, size_range=(1, 80), rate=3.0, seed=33), "relserve-pp", "qwen-32b-like",
+     dict(tau=0.2), 3),
+    (dict(num_relqueries=50, size_range=(1, 80), rate=3.0, seed=34), "relserve-dp", "opt-13b-like",
+     dict(sample_size=5, capacity_blocks=150), 4),
+    (dict(num_relqueries=30, size_range=(1, 120), rate=1.0, seed=35, mean_input_len=64), "relserve",
+     "opt-13b-like", dict(block_size=8, capacity_blocks=90), 5),
+    (dict(num_relqueries=80, size_range=(1, 40), rate=10.0, seed=36), "sp", "opt-13b-like", {}, 0),
+    (dict(num_relqueries=80, size_range=(1, 40), rate=10.0, seed=37), "fcfs", "llama-70b-like",
+     dict(capacity_blocks=200), 0),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_device_matches_oracle_random_traces(case, oracle_mod):
+    from paper_2601_11546_b200 import EngineConfig, SchedulerConstraints, TraceConfig, generate_trace, world_preset
+
+    tc, policy, world, kw, seed = CASES[case]
+    trace = generate_trace(TraceConfig(**tc))
+    cfg = EngineConfig(**kw)
+    w = world_preset(world)
+    ref = oracle_mod.run(trace, policy, w, cfg, None, seed)
+    assert ref.status == 0, ref.message
+    res, aborted = run_device(trace, policy, w, cfg, None, seed)
+    assert aborted is None
+    assert res.iterations == ref.iterations
+    for k in ref.log.dtype.names:
+        a, b = res.records[k], ref.log[k]
+        if a.dtype.kind == "f":
+            assert np.array_equal(a, b, equal_nan=True), k
+        else:
+            assert np.array_equal(a, b), k
+    assert np.array_equal(res.completion_iteration, ref.completion_iter)
+    assert res.sim_duration == ref.clock
+    assert (res.cache_hit_tokens, res.cache_miss_tokens) == (ref.cache_hit_tokens, ref.cache_miss_tokens)

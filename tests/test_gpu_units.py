@@ -1,0 +1,53 @@
+"""Device unit entry points: PEM batch and the numpy choice replay."""
+
+import numpy as np
+import pytest
+
+from paper_2601_11546_b200 import LinearCostModel, SchedulerConstraints, _abi, _native
+
+pytestmark = pytest.mark.gpu
+
+MODEL = LinearCostModel(0.001, 0.02, 0.0002, 0.015)
+
+
+def test_pem_known_answer():
+    c = SchedulerConstraints(cap=1000, max_num_seqs=10, max_num_batched_tokens=500)
+    v = _native.pem_batch(np.array([0, 3]), np.array([100, 60, 40]), np.array([2, 2, 2], np.int32),
+                          np.zeros(3, np.uint8), c, MODEL)
+    assert v[0] == pytest.approx(0.22 + 2 * 0.0156)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pem_batch_matches_oracle(seed, oracle_mod):
+    rs = np.random.default_rng(seed)
+    cons = [SchedulerConstraints(1000, 10, 200), SchedulerConstraints(150, 10, 150),
+            SchedulerConstraints(10_000, 2, 10_000), SchedulerConstraints(200_000, 256, 8192),
+            SchedulerConstraints(4000, 16, 512)][seed % 5]
+    sets = []
+    for _ in range(300):
+        n = int(rs.integers(0, 1500 if seed % 2 else 60))
+        q = int(rs.integers(0, n + 1))
+        pre = np.zeros(n, np.uint8)
+        pre[:q] = 1
+        utok = rs.integers(0, min(cons.cap, 400) + 1, size=n)
+        utok[pre == 1] = 0
+        rem = rs.integers(1, 40, size=n).astype(np.int32)
+        sets.append((utok, rem, pre))
+    off = np.cumsum([0] + [len(s[0]) for s in sets])
+    got = _native.pem_batch(off, np.concatenate([s[0] for s in sets]).astype(np.int64),
+                            np.concatenate([s[1] for s in sets]).astype(np.int32),
+                            np.concatenate([s[2] for s in sets]).astype(np.uint8), cons, MODEL)
+    for i, (u, r, p) in enumerate(sets):
+        assert got[i] == oracle_mod.pem(u, r, p, cons, MODEL), i
+
+
+def test_choice_sequence_matches_numpy():
+    g = np.random.default_rng(np.random.SeedSequence([3, 0xD9]))
+    st = _abi.Pcg64State.from_numpy(g.bit_generator.state)
+    rs = np.random.default_rng(0)
+    ns = rs.integers(2, 5000, size=500)
+    ks = np.minimum(ns - 1, rs.integers(1, 9, size=500))
+    got = _native.choice_sequence(st, ns, ks)
+    want = np.concatenate([g.choice(int(n), size=int(k), replace=False) for n, k in zip(ns, ks)])
+    assert got.tolist() == want.tolist()
+    assert st.to_numpy()["state"] == g.bit_generator.state["state"]
