@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark: scheduler iterations/s at 10^6 pending requests (BASELINE.json).
+
+Workload (config 2 of BASELINE.json): 1,000 relQueries x 1,000 rows
+(10^6 requests, all arriving within ~1 ms), opt-13b-like cost model (the
+only 13B preset; "Llama-2-13B" maps to it), EngineConfig() defaults, policy
+relserve, engine seed 0.  A *step* is one launch of the persistent scheduler
+kernel that advances the trace by `--iters-per-step` scheduler iterations.
+The window starts at iteration 5 (after admission and the first-sight DPU
+pass); W warm-up steps, then K timed steps, each bracketed
+by CUDA events on the launching stream, with a 256 MiB L2 flush between steps
+(outside the events).  `value` = iterations / summed step time.
+
+`e2e` runs the same window through the public API (`Engine` over host
+arrays): trace upload, every step's launch, status and decision-record
+readback, and the final ledger/request readback are inside the wall-clock
+timed region.
+
+`--impl reference` times the CPU restatement of the reference engine
+(oracle/, single-threaded like the reference) on the same trace and window.
+
+Multi-GPU (torchrun, N ranks): every rank runs an independent config-2 trace
+(seed = rank); value = all ranks' iterations / max-over-ranks time (weak
+scaling; a single trace's iterations are serially dependent).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sched iters/sec @1M pending reqs"
+WINDOW_START = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--iters-per-step", type=int, default=2000)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["2", "3"], default="2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=1500)
+    return ap.parse_args()
+
+
+def workload(cfg_id: str, seed: int):
+    from paper_2601_11546_b200 import (EngineConfig, TraceConfig, generate_heavy_tail_trace,
+                                       generate_trace, world_preset)
+
+    if cfg_id == "2":
+        trace = generate_trace(TraceConfig(num_relqueries=1000, size_range=(1000, 1000), rate=1e6, seed=seed))
+        world = world_preset("opt-13b-like")
+        name = "config2: 1000 relQ x 1000 rows, opt-13b-like (Llama-2-13B), relserve"
+    else:
+        trace = generate_heavy_tail_trace(num_relqueries=5000, size_range=(1, 399), rate=1e6, seed=seed)
+        world = world_preset("llama-70b-like")
+        name = "config3: 5000 relQ x U[1,399] heavy-tailed outputs, llama-70b-like (Llama-2-70B), relserve"
+    return trace, world, EngineConfig(), name
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def max_over_ranks(x: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(recs, c) -> float:
+    """Bytes the device scheduler must touch for these iterations (DESIGN.md
+    'Algorithmic bytes'): per iteration 20 B per admitted relQuery (priority,
+    prefilled count, row offsets: the waiting argmin), 12 B per row of each
+    re-estimated relQuery (tok, out, gen: the PEM pass), 16 B per running row
+    (decode: tok, out, gen read + gen write) and 16 B per prefilled row."""
+    sizes = np.diff(c.row_off)
+    mean_size = float(sizes.mean()) if sizes.size else 0.0
+    admitted = c.num_relqueries  # all relQueries arrive within the first iterations
+    total = 0.0
+    for r in recs:
+        total += 20.0 * admitted
+        total += 12.0 * mean_size * float(r["n_reestimated"])
+        total += 16.0 * float(r["batch_n"])
+    return total
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    from paper_2601_11546_b200 import _abi, _marshal
+    from paper_2601_11546_b200._native import NativeEngine
+    from paper_2601_11546_b200.engine import Engine
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    trace, world, cfg, wname = workload(args.config, seed=rank)
+    I = args.iters_per_step
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- device-resident timing (inputs already in HBM)
+    m = _marshal.marshal_trace(trace, cfg.block_size, "relserve", world, None)
+    ne = NativeEngine([m.view], _marshal.make_config(cfg, "relserve"), _marshal.make_model(world),
+                      _marshal.make_model(world), [_marshal.dpu_rng_state(0)], local, log_capacity=I)
+    ne.step(WINDOW_START, stream)
+    st = ne.status(stream)[0]
+    assert st.status == _abi.RS_RUNNING and st.iterations == WINDOW_START, (st.status, st.iterations)
+    n_read = st.n_log
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        ne.step(I, stream)
+    st = ne.status(stream)[0]
+    n_read = st.n_log
+    it0 = st.iterations
+    pending0 = trace.columns().num_requests
+    evs = []
+    recs = []
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ne.step(I, stream)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    st = ne.status(stream)[0]
+    iters = st.iterations - it0
+    assert st.status == _abi.RS_RUNNING, f"trace ended inside the window (status {st.status})"
+    recs = ne.read_log(0, n_read, st.n_log - n_read)
+    gen, pre, comp, prio = ne.read_requests(0, trace.columns().num_requests)
+    pending_end = int((pre == 0).sum())
+    ne.close()
+    t_ms = sum(step_ms)
+    t_max = max_over_ranks(t_ms, ws, dev)
+    total_iters = sum_over_ranks(float(iters), ws, dev)
+    value = total_iters / (t_max / 1e3)
+    c = trace.columns()
+    alg = algorithmic_bytes(recs, c)
+    per_launch_bytes = alg / args.steps
+    avg_launch_s = (t_ms / args.steps) / 1e3
+    peak, peak_kind = peaks()
+    achieved = per_launch_bytes / avg_launch_s / 1e9
+
+    # ---- end to end through the public API (host buffers, copies inside)
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        eng = Engine(trace, "relserve", world, cfg, seed=0, device=local, stream=stream)
+        eng.chunk_iterations = I
+        st0 = eng.step(WINDOW_START)
+        for _ in range(args.steps):
+            eng.step(I)
+        res = eng._collect(0.0)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        e_iters = eng.iteration
+        eng.close()
+        h2d = sum(v.nbytes for v in m.arrays.values() if v is not None)
+        d2h_step = I * 96 + 128
+        d2h_final = c.num_requests * (4 + 1 + 8 + 8) + c.num_relqueries * 32
+        wall_max = max_over_ranks(wall, ws, dev)
+        e2e_total = sum_over_ranks(float(e_iters), ws, dev)
+        e2e = {"value": e2e_total / wall_max, "unit": "iters/s",
+               "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / args.steps),
+               "iterations": int(e_iters), "wall_s": wall_max,
+               "includes": "trace upload, iterations 0..window end (incl. first-sight DPU), per-step record readback, final ledger/request readback"}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and ws == 1:
+            cpu = cpu_baseline(args, trace, world, cfg)
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "iters/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64+int32",
+            "data": "synthetic (relsim generate_trace, count-identical to the reference generator)",
+            "config": {"workload": wname, "iters_per_step": I, "window_start_iteration": WINDOW_START,
+                       "pending_requests_start": pending0, "pending_requests_end": pending_end,
+                       "l2": "256 MiB buffer written between timed steps (outside the events)",
+                       "traces_per_gpu": 1},
+            "iterations_timed": int(total_iters),
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                         "note": "latency-bound serial iteration chain; bytes = DESIGN.md algorithmic bytes"},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+    return out
+
+
+def cpu_baseline(args, trace, world, cfg, iters=None):
+    """Oracle (C restatement of the reference loop, 1 thread) on the same trace."""
+    from dataclasses import replace
+
+    from oracle import oracle
+
+    iters = iters or args.cpu_iters
+    c2 = replace(cfg, iteration_limit=WINDOW_START + iters)
+    t0 = time.perf_counter()
+    r = oracle.run(trace, "relserve", world, c2, None, 0)
+    wall = time.perf_counter() - t0
+    win = r.iter_wall[WINDOW_START:WINDOW_START + iters]
+    return {"value": float(len(win) / win.sum()), "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": f"iterations [{WINDOW_START}, {WINDOW_START + len(win)}) of the same trace "
+                      f"(steady state; first-sight iteration {r.first_sight_iter} took "
+                      f"{r.first_sight_wall_s:.3f} s); run wall {wall:.1f} s",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    trace, world, cfg, wname = workload(args.config, seed=0)
+    per_step = max(1, args.iters_per_step // 20)
+    n = WINDOW_START + (args.warmup + args.steps) * per_step
+    from dataclasses import replace
+
+    from oracle import oracle
+
+    r = oracle.run(trace, "relserve", world, replace(cfg, iteration_limit=n), None, 0)
+    lo = WINDOW_START + args.warmup * per_step
+    win = r.iter_wall[lo:n]
+    value = float(len(win) / win.sum())
+    return {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(win.sum() / args.steps * 1e3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
+        "config": {"workload": wname, "iters_per_step": per_step, "window_start_iteration": lo},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle/ C restatement of relsim Engine.run, iterations [{lo}, {n})",
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        out = run_ours(args, ws, rank, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -149,7 +149,7 @@ struct Shared {
   int n_dist, act_dirty;
   int dist[kMaxRun];
   int sorted_dist[kMaxRun];
-  unsigned char pem_smem[pem_bytes_per_item() * kPemSmemItems + 16];
+  alignas(16) unsigned char pem_smem[pem_bytes_per_item() * kPemSmemItems + 16];
 };
 
 __device__ __forceinline__ unsigned long long dbits(double x) {

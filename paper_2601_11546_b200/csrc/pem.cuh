@@ -62,8 +62,9 @@ __host__ __device__ inline PemBuf pem_carve(void* base, int cap_items) {
   return b;
 }
 
+// rounded to 16 bytes so per-CTA slices of one allocation stay 8-byte aligned
 __host__ __device__ inline size_t pem_buf_size(int cap_items) {
-  return pem_bytes_per_item() * (size_t)cap_items + 16;
+  return (pem_bytes_per_item() * (size_t)cap_items + 16 + 15) & ~(size_t)15;
 }
 
 struct PemShared {
