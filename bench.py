@@ -203,7 +203,8 @@ def run_ours(args, ws, rank, local):
     # ---- device-resident timing (inputs already in HBM)
     m = _marshal.marshal_trace(trace, cfg.block_size, "relserve", world, None)
     ne = NativeEngine([m.view], _marshal.make_config(cfg, "relserve"), _marshal.make_model(world),
-                      _marshal.make_model(world), [_marshal.dpu_rng_state(0)], local, log_capacity=I)
+                      _marshal.make_model(world), [_marshal.dpu_rng_state(0)], local,
+                      log_capacity=I * (args.steps + args.warmup + 1) + WINDOW_START)
     ne.step(WINDOW_START, stream)
     st = ne.status(stream)[0]
     assert st.status == _abi.RS_RUNNING and st.iterations == WINDOW_START, (st.status, st.iterations)
@@ -214,6 +215,7 @@ def run_ours(args, ws, rank, local):
     st = ne.status(stream)[0]
     n_read = st.n_log
     it0 = st.iterations
+    ph0 = list(st.phase_cycles)
     pending0 = trace.columns().num_requests
     evs = []
     recs = []
@@ -237,6 +239,7 @@ def run_ours(args, ws, rank, local):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     st = ne.status(stream)[0]
     iters = st.iterations - it0
+    ph = [a - b for a, b in zip(st.phase_cycles, ph0)]
     assert st.status == _abi.RS_RUNNING, f"trace ended inside the window (status {st.status})"
     recs = ne.read_log(0, n_read, st.n_log - n_read)
     gen, pre, comp, prio = ne.read_requests(0, trace.columns().num_requests)
@@ -307,6 +310,10 @@ def run_ours(args, ws, rank, local):
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
                          "note": "latency-bound serial iteration chain; bytes = DESIGN.md algorithmic bytes"},
             "clocks": clk.summary(),
+            "phase_share": dict(zip(("admit", "dpu", "order", "arrange", "execute"),
+                                    [round(x / max(1, sum(ph)), 4) for x in ph])),
+            "phase_cycles_per_iter": dict(zip(("admit", "dpu", "order", "arrange", "execute"),
+                                              [round(x / max(1, iters), 1) for x in ph])),
             "cpu_baseline": cpu,
         }
     return out

@@ -56,6 +56,7 @@ constexpr int kMaxRun = 1024;      // device limit on max_num_seqs
 constexpr int kMaxAct = 1024;      // partially-prefilled live relQueries
 constexpr int kMaxCC = 256;        // tail-less resident chains
 constexpr int kPemSmemItems = 1024;
+constexpr int kWin = 768;          // FIFO window of the batched prefill eviction
 
 struct FifoEnt {
   unsigned long long t0;  // touch time of the tail's first block
@@ -66,7 +67,7 @@ struct FifoEnt {
 struct CcEnt {
   unsigned long long key;  // touch time of the chain's last resident block
   int rank;
-  int pad;
+  int m;                   // resident chain blocks
 };
 
 // Persistent per-trace control block (global between launches, shared during one).
@@ -84,9 +85,12 @@ struct alignas(16) Ctl {
   int status, error_detail;
   int cc_n, pad;
   rs_pcg64_state rng;
+  long long phase[6];  // clock64 cycles per phase (+ scratch timestamp in [5])
   int run_row[kMaxRun];
   int run_rank[kMaxRun];
   int act[kMaxAct];
+  int rrq[kMaxRun];  // relQueries with running rows (distinct)
+  int n_rrq, pad2[3];
   CcEnt cc[kMaxCC];
 };
 
@@ -108,6 +112,7 @@ struct TraceDev {
   int* m;       // resident chain blocks
   unsigned long long* c0;
   int* ntails;  // rows of this relQuery with a resident tail
+  int* nrun;    // running rows of this relQuery
   double* fps;
   double* lpe;
   double* lde;
@@ -117,6 +122,8 @@ struct TraceDev {
   long long fifo_cap;
   int* est;
   double* ratio;
+  int* scr_cnt;   // [R] zeroed scratch: window tails per relQuery
+  int* scr_last;  // [R] scratch (-1): last window index per relQuery
   void* pem_global;  // PemBuf backing for relQueries larger than kPemSmemItems
   rs_iter_record* log;
   long long log_cap;
@@ -146,10 +153,23 @@ struct Shared {
   long long utok_sum;
   double m_plus, m_minus;
   int dmin_slot, n_est;
-  int n_dist, act_dirty;
-  int dist[kMaxRun];
+  int n_dist, act_dirty, rrq_dirty;
   int sorted_dist[kMaxRun];
-  alignas(16) unsigned char pem_smem[pem_bytes_per_item() * kPemSmemItems + 16];
+  // batched prefill eviction
+  int fp_bad, fp_ok, fp_popped, fp_win;
+  long long fp_E;
+  unsigned long long fp_c0_last;
+  union {
+    alignas(16) unsigned char pem_smem[pem_bytes_per_item() * kPemSmemItems + 16];
+    struct {
+      unsigned long long t0[kWin];
+      unsigned long long c0[kWin];
+      int rank[kWin];
+      int tres[kWin];
+      int mm[kWin];
+      int last[kWin];  // 1 if this is the rank's last resident tail
+    } win;
+  };
 };
 
 __device__ __forceinline__ unsigned long long dbits(double x) {
@@ -159,24 +179,25 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7FF8000000000000LL); }
 
 // ---------------------------------------------------------------------------
-// Prefix-cache LRU model (single thread)
+// Prefix-cache LRU model
+//
+// cc[] holds exactly the resident chains that have no resident tails (the
+// only chain blocks that can be LRU leaves), sorted by the touch time of
+// their last resident block.  An entry is removed as soon as its relQuery is
+// prefilled again, so entries never go stale and carry their own length.
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ bool cc_valid(const TraceDev& T, const CcEnt& e) {
-  const int a = e.rank;
-  const int mm = T.m[a];
-  return T.ntails[a] == 0 && mm > 0 && T.c0[a] + (unsigned long long)(mm - 1) == e.key;
+__device__ __forceinline__ void cc_remove(Ctl& c, int rank) {
+  for (int i = 0; i < c.cc_n; ++i)
+    if (c.cc[i].rank == rank) {
+      for (int j = i + 1; j < c.cc_n; ++j) c.cc[j - 1] = c.cc[j];
+      c.cc_n--;
+      return;
+    }
 }
 
-// Insert a chain candidate keeping cc sorted by key; drops stale entries when full.
-__device__ bool cc_insert(Ctl& c, const TraceDev& T, unsigned long long key, int rank) {
-  if (c.cc_n == kMaxCC) {
-    int w = 0;
-    for (int i = 0; i < c.cc_n; ++i)
-      if (cc_valid(T, c.cc[i])) c.cc[w++] = c.cc[i];
-    c.cc_n = w;
-    if (w == kMaxCC) return false;
-  }
+__device__ __forceinline__ bool cc_insert(Ctl& c, unsigned long long key, int rank, int m) {
+  if (c.cc_n == kMaxCC) return false;
   int pos = c.cc_n;
   while (pos > 0 && c.cc[pos - 1].key > key) {
     c.cc[pos] = c.cc[pos - 1];
@@ -184,18 +205,29 @@ __device__ bool cc_insert(Ctl& c, const TraceDev& T, unsigned long long key, int
   }
   c.cc[pos].key = key;
   c.cc[pos].rank = rank;
+  c.cc[pos].m = m;
   c.cc_n++;
   return true;
 }
 
-// Evict until count <= C.  cur_rank/cur_tail identify the pinned path (the
-// row just inserted): its chain and, if it has one, its tail (the FIFO back).
+// Evict the chain candidate at the front: k blocks from its end.
+__device__ __forceinline__ void cc_evict_front(Ctl& c, const TraceDev& T, long long k) {
+  CcEnt& e = c.cc[0];
+  e.m -= (int)k;
+  e.key -= (unsigned long long)k;
+  T.m[e.rank] = e.m;
+  c.count -= k;
+  if (e.m == 0) {
+    for (int i = 1; i < c.cc_n; ++i) c.cc[i - 1] = c.cc[i];
+    c.cc_n--;
+  }
+}
+
+// Exact per-row eviction (single thread): evict until count <= C.  cur_rank /
+// cur_tail identify the pinned path (the row just inserted): its chain and,
+// if it has one, its tail (the FIFO back).
 __device__ int cache_evict(Ctl& c, const TraceDev& T, long long C, int cur_rank, bool cur_tail) {
   while (c.count > C) {
-    while (c.cc_n > 0 && !cc_valid(T, c.cc[0])) {
-      for (int i = 1; i < c.cc_n; ++i) c.cc[i - 1] = c.cc[i];
-      c.cc_n--;
-    }
     const bool have_f = c.fifo_head < c.fifo_tail;
     unsigned long long kf = ~0ULL, kc = ~0ULL;
     FifoEnt fe;
@@ -216,32 +248,24 @@ __device__ int cache_evict(Ctl& c, const TraceDev& T, long long C, int cur_rank,
         const int a = fe.rank;
         const int nt = T.ntails[a] - 1;
         T.ntails[a] = nt;
-        if (nt == 0 && T.m[a] > 0) {
-          if (!cc_insert(c, T, T.c0[a] + (unsigned long long)(T.m[a] - 1), a)) return RS_EUNSUPPORTED;
-        }
+        const int mm = T.m[a];
+        if (nt == 0 && mm > 0 && !cc_insert(c, T.c0[a] + (unsigned long long)(mm - 1), a, mm))
+          return RS_EUNSUPPORTED;
       } else {
         T.fifo[c.fifo_head % T.fifo_cap].tres = fe.tres;
       }
     } else {
-      const int a = c.cc[0].rank;
-      if (a == cur_rank) return RS_ECACHE_PINNED;
-      const int mm = T.m[a];
-      const long long k = need < mm ? need : mm;
-      T.m[a] = mm - (int)k;
-      c.count -= k;
-      if (mm - k == 0) {
-        for (int i = 1; i < c.cc_n; ++i) c.cc[i - 1] = c.cc[i];
-        c.cc_n--;
-      } else {
-        c.cc[0].key -= (unsigned long long)k;
-      }
+      if (c.cc[0].rank == cur_rank) return RS_ECACHE_PINNED;
+      const long long k = need < c.cc[0].m ? need : c.cc[0].m;
+      cc_evict_front(c, T, k);
     }
   }
   return RS_OK;
 }
 
-// match_uncached(refresh=True, record=True) + insert for one row (engine.py:321-323).
-// Returns the row's uncached tokens, or -1 on error (status set).
+// Exact path for one row: match_uncached(refresh=True, record=True) + insert
+// (engine.py:321-323, prefix_cache.py:70-120).  Returns the row's uncached
+// tokens, or -1 on error (status set).
 __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const Params& P, int a, int row) {
   const long long B = P.cfg.block_size;
   const int tok = T.tok[row];
@@ -250,6 +274,7 @@ __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const Params& 
   const int T_len = nb - Pc;
   const int mb = T.m[a];
   const long long hit = B * mb;
+  cc_remove(c, a);                                    // the chain is touched again
   c.hit += hit;
   c.miss += tok - hit;
   c.tclock += (unsigned long long)mb;                 // match touches the resident chain
@@ -269,7 +294,7 @@ __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const Params& 
     c.fifo_tail++;
     T.ntails[a] += 1;
   } else if (Pc > 0 && T.ntails[a] == 0) {
-    if (!cc_insert(c, T, c0 + (unsigned long long)(Pc - 1), a)) {
+    if (!cc_insert(c, c0 + (unsigned long long)(Pc - 1), a, Pc)) {
       c.status = RS_EUNSUPPORTED;
       c.error_detail = 1;
       return -1;
@@ -282,6 +307,147 @@ __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const Params& 
     return -1;
   }
   return tok - hit;
+}
+
+
+// Batched prefill advance (all threads).  All rows of a prefill batch belong
+// to the head relQuery h, whose chain is pinned by every row's insert and is
+// fully resident after the first one; if every row also has a private tail,
+// the reference's per-row insert/evict interleaving evicts, in LRU order, the
+// first E = max(0, count + new - C) blocks of the pre-batch resident set --
+// whatever the interleaving, as long as E does not exceed those blocks.  So:
+// per-row touch times and FIFO pushes by prefix sums, then one thread walks
+// the FIFO head (staged in shared memory) and the chain candidates for E
+// blocks.  Returns false (nothing changed) when the preconditions fail; the
+// caller then runs the exact per-row path.
+__device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int h, int off, int q, int n,
+                             long long& ut_out) {
+  Ctl& c = S.c;
+  const int tid = threadIdx.x;
+  const long long B = P.cfg.block_size;
+  const long long C = P.cfg.capacity_blocks;
+  const int Pc = T.chain[h];
+  const int m0 = T.m[h];
+  const unsigned long long tc = c.tclock;
+  const long long head0 = c.fifo_head, tail0 = c.fifo_tail, count0 = c.count;
+  if (tid == 0) S.fp_bad = 0;
+  __syncthreads();
+  long long tokv[kMaxRun / kThreads], Tv[kMaxRun / kThreads], inclT[kMaxRun / kThreads];
+  long long cT = 0, cTok = 0;
+#pragma unroll
+  for (int s = 0; s < kMaxRun / kThreads; ++s) {
+    const int i = s * kThreads + tid;
+    tokv[s] = 0;
+    Tv[s] = 0;
+    if (i < n) {
+      tokv[s] = T.tok[off + q + i];
+      Tv[s] = tokv[s] / B - Pc;
+      if (Tv[s] <= 0) S.fp_bad = 1;
+    }
+    long long v[2] = {Tv[s], tokv[s]}, tot[2];
+    block_incl_scan<2>(v, S.scan, tot);
+    inclT[s] = cT + v[0];
+    cT += tot[0];
+    cTok += tot[1];
+  }
+  const long long newn = (long long)(Pc - m0) + cT;
+  const long long E = count0 + newn > C ? count0 + newn - C : 0;
+  const long long n_old = tail0 - head0;
+  const int Wn = (int)(E < n_old ? E : n_old);
+  if (S.fp_bad || E > count0 - m0 || Wn > kWin) return false;
+  // FIFO pushes: row i's chain/tail touch times from prefix sums of touches
+#pragma unroll
+  for (int s = 0; s < kMaxRun / kThreads; ++s) {
+    const int i = s * kThreads + tid;
+    if (i < n) {
+      const long long before = i == 0 ? 0 : (long long)m0 + (long long)(i - 1) * Pc + (long long)i * Pc + (inclT[s] - Tv[s]);
+      const long long mb = i == 0 ? m0 : Pc;
+      const unsigned long long c0i = tc + (unsigned long long)(before + mb + 1);
+      FifoEnt e;
+      e.t0 = c0i + (unsigned long long)Pc;
+      e.rank = h;
+      e.tres = (int)Tv[s];
+      T.fifo[(tail0 + i) % T.fifo_cap] = e;
+      if (i == n - 1) S.fp_c0_last = c0i;
+    }
+  }
+  // stage the FIFO head (the oldest tails) and their relQueries' chain state
+  for (int j = tid; j < Wn; j += kThreads) {
+    const FifoEnt e = T.fifo[(head0 + j) % T.fifo_cap];
+    S.win.t0[j] = e.t0;
+    S.win.rank[j] = e.rank;
+    S.win.tres[j] = e.tres;
+    S.win.mm[j] = T.m[e.rank];
+    S.win.c0[j] = T.c0[e.rank];
+    atomicAdd(&T.scr_cnt[e.rank], 1);
+    atomicMax(&T.scr_last[e.rank], j);
+  }
+  __syncthreads();
+  for (int j = tid; j < Wn; j += kThreads) {
+    const int a = S.win.rank[j];
+    S.win.last[j] = (a != h && T.scr_last[a] == j && T.scr_cnt[a] == T.ntails[a]) ? 1 : 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    cc_remove(c, h);
+    long long need = E;
+    int j = 0;
+    bool ok = true;
+    while (need > 0) {
+      const unsigned long long kf = j < Wn ? S.win.t0[j] + (unsigned long long)(S.win.tres[j] - 1) : ~0ULL;
+      const unsigned long long kc = c.cc_n > 0 ? c.cc[0].key : ~0ULL;
+      if (kf == ~0ULL && kc == ~0ULL) {
+        ok = false;
+        break;
+      }
+      if (kf < kc) {
+        const long long k = need < S.win.tres[j] ? need : S.win.tres[j];
+        S.win.tres[j] -= (int)k;
+        need -= k;
+        c.count -= k;
+        if (S.win.tres[j] == 0) {
+          const int mm = S.win.mm[j];
+          if (S.win.last[j] && mm > 0 &&
+              !cc_insert(c, S.win.c0[j] + (unsigned long long)(mm - 1), S.win.rank[j], mm)) {
+            ok = false;
+            break;
+          }
+          ++j;
+        }
+      } else {
+        const long long k = need < c.cc[0].m ? need : c.cc[0].m;
+        need -= k;
+        cc_evict_front(c, T, k);
+      }
+    }
+    if (!ok) {
+      c.status = RS_ECACHE_PINNED;
+      c.error_detail = 4;
+    }
+    if (j < Wn) T.fifo[(head0 + j) % T.fifo_cap].tres = S.win.tres[j];
+    S.fp_popped = j;
+    const long long hitb = (long long)m0 + (long long)(n - 1) * Pc;
+    c.hit += B * hitb;
+    c.miss += cTok - B * hitb;
+    ut_out = cTok - B * hitb;
+    c.tclock = tc + (unsigned long long)(hitb + (long long)n * Pc + cT);
+    c.count += newn;
+    c.fifo_head = head0 + j;
+    c.fifo_tail = tail0 + n;
+    T.m[h] = Pc;
+    T.c0[h] = S.fp_c0_last;
+  }
+  __syncthreads();
+  const int popped = S.fp_popped;
+  for (int j = tid; j < Wn; j += kThreads) {
+    const int a = S.win.rank[j];
+    if (j < popped) atomicSub(&T.ntails[a], 1);
+    T.scr_cnt[a] = 0;
+    T.scr_last[a] = -1;
+  }
+  if (tid == 0) atomicAdd(&T.ntails[h], n);
+  __syncthreads();
+  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -343,6 +509,15 @@ __device__ double sample_ratio(Pcg64& g, const TraceDev& T, const Params& P, int
   return __ddiv_rn((double)usum, (double)tsum);
 }
 
+// thread 0 accumulates the cycles since the previous mark into phase k
+__device__ __forceinline__ void phase_mark(Ctl& c, int k) {
+  if (threadIdx.x == 0) {
+    const long long now = clock64();
+    c.phase[k] += now - c.phase[5];
+    c.phase[5] = now;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // One scheduler iteration.  Returns false when the trace stopped.
 // ---------------------------------------------------------------------------
@@ -377,6 +552,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   }
   __syncthreads();
   if (!S.go) return false;
+  phase_mark(c, 0);
 
   // ---- B: Dynamic Priority Updater (priority.py:287-339)
   if (P.use_dpu) {
@@ -434,6 +610,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   } else if (tid == 0) {
     S.n_est = 0;
   }
+  phase_mark(c, 1);
 
   // ---- C: waiting head = argmin (prio, rank) over relQueries with pending rows
   {
@@ -454,6 +631,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       S.head = W > 0 ? (int)idx : -1;
     }
   }
+  phase_mark(c, 2);
 
   // ---- D: candidates (engine.py:285-308)
   {
@@ -523,27 +701,15 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   bool need_proj = false;
   if (!P.prefill_first && has_p && has_d && S.m_plus <= S.m_minus) need_proj = true;
   if (need_proj) {
-    // distinct running relQueries, sorted by rel_id (engine.py:406-408)
-    if (tid == 0) S.n_dist = 0;
-    __syncthreads();
-    for (int j = tid; j < c.n_run; j += kThreads) {
-      const int a = c.run_rank[j];
-      bool first = true;
-      for (int k = 0; k < j; ++k)
-        if (c.run_rank[k] == a) {
-          first = false;
-          break;
-        }
-      if (first) S.dist[atomicAdd(&S.n_dist, 1)] = a;
-    }
-    __syncthreads();
-    const int nd = S.n_dist;
+    // distinct running relQueries (the rrq list), sorted by rel_id (engine.py:406-408)
+    const int nd = c.n_rrq;
     for (int i = tid; i < nd; i += kThreads) {
-      const long long ri = T.rel_id[S.dist[i]];
+      const long long ri = T.rel_id[c.rrq[i]];
       int pos = 0;
-      for (int k = 0; k < nd; ++k) pos += T.rel_id[S.dist[k]] < ri;
-      S.sorted_dist[pos] = S.dist[i];
+      for (int k = 0; k < nd; ++k) pos += T.rel_id[c.rrq[k]] < ri;
+      S.sorted_dist[pos] = c.rrq[i];
     }
+    if (tid == 0) S.n_dist = nd;
     __syncthreads();
   }
   if (tid == 0) {
@@ -626,35 +792,36 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   }
   __syncthreads();
   const int action = S.go;
+  phase_mark(c, 3);
 
   // ---- F: execute
   if (action == RS_ACTION_PREFILL) {  // _execute_prefill (engine.py:315-341)
+    const int h = S.head;
+    const int off = T.row_off[h];
+    const int q = T.q[h];
+    const int n = S.taken;
+    const int n_run0 = c.n_run;
+    long long ut = 0;
+    const bool fast = prefill_fast(P, T, S, h, off, q, n, ut);
     if (tid == 0) {
-      const int h = S.head;
-      const int off = T.row_off[h];
-      const int q = T.q[h];
-      const int n = S.taken;
-      const double start = c.clock;
-      long long ut = 0;
-      bool ok = true;
-      for (int i = 0; i < n; ++i) {
-        const long long u = prefill_row_cache(c, T, P, h, off + q + i);
-        if (u < 0) {
-          ok = false;
-          break;
+      bool ok = c.status == RS_RUNNING;
+      if (!fast && ok) {
+        for (int i = 0; i < n; ++i) {
+          const long long u = prefill_row_cache(c, T, P, h, off + q + i);
+          if (u < 0) {
+            ok = false;
+            break;
+          }
+          ut += u;
         }
-        ut += u;
       }
       if (ok) {
+        const double start = c.clock;
         const double dur = __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p);
-        const int ol = T.ol[h];
-        for (int i = 0; i < n; ++i) {
-          c.run_row[c.n_run] = off + q + i;
-          c.run_rank[c.n_run] = h;
-          c.n_run++;
-          c.kv += (long long)T.tok[off + q + i] + ol;
-        }
+        c.n_run = n_run0 + n;
         T.q[h] = q + n;
+        if (T.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
+        T.nrun[h] += n;
         if (q == 0 && P.use_dpu) {  // becomes partially prefilled: join the re-estimate list
           int pos = c.n_act;
           if (pos >= kMaxAct) {
@@ -681,12 +848,26 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       }
       S.go = ok && c.status == RS_RUNNING;
     }
+    // running list append + kv reservation (engine.py:326-329)
+    long long kv = 0;
+    const int ol = T.ol[h];
+    for (int i = tid; i < n; i += kThreads) {
+      c.run_row[n_run0 + i] = off + q + i;
+      c.run_rank[n_run0 + i] = h;
+      kv += (long long)T.tok[off + q + i] + ol;
+    }
+    kv = block_sum(kv, S.scan);
+    if (tid == 0) c.kv += kv;
     __syncthreads();
     if (!S.go) return false;
   } else if (action == RS_ACTION_DECODE) {  // _execute_decode (engine.py:343-363)
     const int n = c.n_run;
     double clk = 0;
-    if (tid == 0) S.act_dirty = 0;
+    if (tid == 0) {
+      S.act_dirty = 0;
+      S.rrq_dirty = 0;
+    }
+    __syncthreads();
     clk = __dadd_rn(c.clock, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d));
     long long kv_free = 0;
     int keep_flag[kMaxRun / kThreads];
@@ -701,6 +882,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         T.gen[r] = g;
         if (g >= T.out[r]) {
           T.comp[r] = (int)c.iteration;
+          if (atomicSub(&T.nrun[a], 1) == 1) S.rrq_dirty = 1;
           kv_free += (long long)T.tok[r] + T.ol[a];
           const int size = T.row_off[a + 1] - T.row_off[a];
           if (atomicAdd(&T.ndone[a], 1) + 1 == size) {
@@ -741,6 +923,12 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       c.kv -= kv_free;
       c.clock = clk;
       if (cfg.log_decisions && T.log_cap > 0) T.log[c.n_log % T.log_cap].batch_n = n;
+      if (S.rrq_dirty) {
+        int w = 0;
+        for (int i = 0; i < c.n_rrq; ++i)
+          if (T.nrun[c.rrq[i]] > 0) c.rrq[w++] = c.rrq[i];
+        c.n_rrq = w;
+      }
       if (S.act_dirty && P.use_dpu) {  // drop retired relQueries from the re-estimate list
         int w = 0;
         for (int i = 0; i < c.n_act; ++i) {
@@ -775,6 +963,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     c.iteration++;
   }
+  phase_mark(c, 4);
   __syncthreads();
   return true;
 }
@@ -790,6 +979,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   }
   __syncthreads();
   if (S.c.status != RS_RUNNING) return;
+  if (threadIdx.x == 0) S.c.phase[5] = clock64();
   for (long long it = 0; it < P.max_iters; ++it)
     if (!iterate(P, T, S)) break;
   __syncthreads();
@@ -1016,16 +1206,19 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_pc
   TRY(dalloc(h, &d.m, R, nullptr, 0));
   TRY(dalloc(h, &d.c0, R, nullptr, 0));
   TRY(dalloc(h, &d.ntails, R, nullptr, 0));
+  TRY(dalloc(h, &d.nrun, R, nullptr, 0));
   std::vector<double> nanv(R, NAN);
   TRY(dalloc(h, &d.fps, R, nanv.data()));
   TRY(dalloc(h, &d.lpe, R, nanv.data()));
   TRY(dalloc(h, &d.lde, R, nanv.data()));
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
-  d.fifo_cap = cfg->capacity_blocks + 2;
+  d.fifo_cap = cfg->capacity_blocks + kMaxRun + 2;  // batched pushes precede evictions
   TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
   TRY(dalloc(h, &d.est, R + kMaxAct, nullptr, 0));
   TRY(dalloc(h, &d.ratio, R + kMaxAct, nullptr, 0));
+  TRY(dalloc(h, &d.scr_cnt, R, nullptr, 0));
+  TRY(dalloc(h, &d.scr_last, R, nullptr, 0xFF));
   if (max_size > kPemSmemItems) {
     TRY(dalloc(h, (unsigned char**)&d.pem_global, pem_buf_size(max_size), nullptr, 0));
   }
@@ -1120,6 +1313,7 @@ int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* st) {
     s.status = c->status;
     s.error_detail = c->error_detail;
     s.rng = c->rng;
+    for (int k = 0; k < 5; ++k) s.phase_cycles[k] = c->phase[k];
   }
   return RS_OK;
 }
