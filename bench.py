@@ -42,6 +42,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "sched iters/sec @1M pending reqs"
+PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dpu_rng", "dpu_ratio_prefix",
+          "dpu_pem", "fp_evict_post", "prefill_post", "cand_decode", "cand_prefill", "fp_scan", "fp_stage")
 WINDOW_START = 5
 
 
@@ -310,10 +312,10 @@ def run_ours(args, ws, rank, local):
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
                          "note": "latency-bound serial iteration chain; bytes = DESIGN.md algorithmic bytes"},
             "clocks": clk.summary(),
-            "phase_share": dict(zip(("admit", "dpu", "order", "arrange", "execute"),
-                                    [round(x / max(1, sum(ph)), 4) for x in ph])),
-            "phase_cycles_per_iter": dict(zip(("admit", "dpu", "order", "arrange", "execute"),
-                                              [round(x / max(1, iters), 1) for x in ph])),
+            "phase_cycles_per_iter": dict(zip(PHASES, [round(x / max(1, iters), 1) for x in ph])),
+            "iteration_mix": {"prefill": int((recs["action"] == 0).sum()), "decode": int((recs["action"] == 1).sum()),
+                              "idle": int((recs["action"] == 2).sum()),
+                              "reestimated_per_iter": float(recs["n_reestimated"].mean()) if len(recs) else 0.0},
             "cpu_baseline": cpu,
         }
     return out

@@ -132,9 +132,10 @@ typedef struct {
   int32_t status;              /* RS_RUNNING, RS_OK (finished) or an error code */
   int32_t error_detail;
   rs_pcg64_state rng;          /* DPU RNG state */
-  /* device clock64() cycles per phase, summed over iterations: admission,
-     priority update (DPU), waiting order, candidates + decision (ABA), execution */
-  int64_t phase_cycles[5];
+  /* device clock64() cycles per phase, summed over iterations: [0] admission,
+     [1] priority update (DPU) remainder, [2] waiting order, [3] candidates +
+     decision (ABA), [4] execution; finer marks [5..14] (see bench.py PHASES) */
+  int64_t phase_cycles[15];
 } rs_trace_status;
 
 typedef struct rs_engine rs_engine;

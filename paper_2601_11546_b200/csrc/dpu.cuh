@@ -1,0 +1,306 @@
+// dpu.cuh -- the Dynamic Priority Updater (priority.py:238-339) for one
+// scheduler iteration, run by the whole CTA.
+//
+// Only relQueries the reference would re-estimate are touched: its reuse rule
+// (priority.py:261-266) keeps the previous value for every live relQuery that
+// was live last time and has no prefilled or finished row, so the estimated
+// set is the partially prefilled live relQueries (the sorted act list) plus
+// this iteration's arrivals, in admission order -- the order the numpy RNG
+// stream is consumed in.  Per batch of up to kEstBatch relQueries:
+//   1. metadata + draw offsets (block scan);
+//   2. sample_cache_miss_ratio's Generator.choice draws for the whole batch
+//      in parallel from PCG64 jump-ahead, with a sequential replay if any
+//      Lemire rejection occurred;
+//   3. ratios (Floyd's set per relQuery; utok of an unprefilled row is
+//      tok - B*m exactly, prefix_cache.py:70-93);
+//   4. PEM: running rows enter as a prefilled summary, unprefilled rows as
+//      utok_approx items; segment-parallel (seg_pem.cuh) when segments can
+//      only close by count, else one warp per relQuery (warp_pem.cuh).
+// Then the starvation override for wholly-waiting relQueries.
+#pragma once
+#include "engine_state.cuh"
+
+namespace rsd {
+
+// Unprefilled rows [q, size) of a relQuery as PEM items (remainder_items,
+// priority.py:81-98): utok_approx = min(tok, floor(tok*ratio + 0.5))
+// (prefix_cache.py:172-176), remaining = output_limit, not prefilled.
+__device__ __forceinline__ long long utok_approx(long long tk, double ratio) {
+  const long long a = (long long)floor(__dadd_rn(__dmul_rn((double)tk, ratio), 0.5));
+  return tk < a ? tk : a;
+}
+
+struct UnprefItems {
+  const int* tok;
+  int base, ol;
+  double ratio;
+  __device__ __forceinline__ void item(int t, long long& u, int& rem, int& pre) const {
+    u = utok_approx(tok[base + t], ratio);
+    rem = ol;
+    pre = 0;
+  }
+};
+
+struct EstItems {
+  const int* tok;
+  const int* off;
+  const int* q;
+  const int* nunp;
+  const int* ol;
+  const double* ratio;
+  __device__ __forceinline__ int count(int e) const { return nunp[e]; }
+  __device__ __forceinline__ void item(int e, int i, long long& u, int& rem, int& pre) const {
+    u = utok_approx(tok[off[e] + q[e] + i], ratio[e]);
+    rem = ol[e];
+    pre = 0;
+  }
+};
+
+struct PrioOut {
+  double* prio;
+  const int* rank;
+  __device__ __forceinline__ void operator()(int e, double v) const { prio[rank[e]] = v; }
+};
+
+// Sequential sample_cache_miss_ratio (prefix_cache.py:141-169) for relQuery a
+// (thread 0; the fallback after a Lemire rejection).
+__device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq, const Params& P, int a) {
+  const int off = rq.off[a];
+  const int size = rq.off[a + 1] - off;
+  const int q = rq.q[a];
+  const int n = size - q;  // unprefilled rows = [q, size) (SURVEY A-inv1)
+  if (n <= 0) return 0.0;
+  const long long mh = P.cfg.block_size * (long long)rq.m[a];
+  const int k = (int)(P.cfg.sample_size < n ? P.cfg.sample_size : n);
+  long long usum = 0, tsum = 0;
+  if (k < n) {
+    uint32_t idx[kMaxSample];
+    choice_floyd(g, (uint32_t)n, (uint32_t)k, idx);
+    for (int i = 0; i < k; ++i) {
+      const long long t = T.tok[off + q + (int)idx[i]];
+      usum += t - mh;
+      tsum += t;
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      const long long t = T.tok[off + q + i];
+      usum += t - mh;
+      tsum += t;
+    }
+  }
+  return __ddiv_rn((double)usum, (double)tsum);
+}
+
+__device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const rs_config& cfg = P.cfg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_act = c.n_act;
+  const int n_new = S.new_hi - S.new_lo;
+  const int n_est = n_act + n_new;
+  const int Ssz = (int)cfg.sample_size;
+  const int dper = 2 * Ssz - 1;  // next32 draws of one choice(n, k=S) call without rejection
+  const int batch = kDrawBuf / dper < kEstBatch ? (kDrawBuf / dper > 0 ? kDrawBuf / dper : 1) : kEstBatch;
+  const long long B = cfg.block_size;
+  PemModel pm;
+  pm.ap = P.pol.alpha_p;
+  pm.bp = P.pol.beta_p;
+  pm.ad = P.pol.alpha_d;
+  pm.bd = P.pol.beta_d;
+  pm.cap = cfg.cap;
+  pm.mns = cfg.max_num_seqs;
+  pm.mnbt = cfg.max_num_batched_tokens;
+  if (tid == 0) S.n_est = n_est;
+  for (int b0 = 0; b0 < n_est; b0 += batch) {
+    const int nb = n_est - b0 < batch ? n_est - b0 : batch;
+    // 1. metadata and draw offsets
+    long long dcount = 0;
+    if (tid < nb) {
+      const int e = b0 + tid;
+      const int a = e < n_act ? c.act[e] : S.new_lo + (e - n_act);
+      const int off = rq.off[a];
+      const int size = rq.off[a + 1] - off;
+      const int q = rq.q[a];
+      S.est_rank[tid] = a;
+      S.est_off[tid] = off;
+      S.est_q[tid] = q;
+      S.est_nunp[tid] = size - q;
+      S.est_ol[tid] = rq.ol[a];
+      S.est_m[tid] = rq.m[a];
+      dcount = size - q > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
+    }
+    {
+      long long v[1] = {dcount}, tot[1];
+      block_incl_scan<1>(v, S.scan, tot);
+      if (tid < nb) S.est_doff[tid] = (int)(v[0] - dcount);
+      if (tid == 0) {
+        S.est_doff[nb] = (int)tot[0];
+        S.rng_reject = 0;
+      }
+    }
+    __syncthreads();
+    phase_mark(c, 5);
+    // 2. numpy's next32 stream, position p -> bounded draw, in parallel
+    const int D = S.est_doff[nb];
+    const unsigned h0 = c.rng.has_uint32;
+    const U128 s0{c.rng.state_hi, c.rng.state_lo};
+    {
+      const int ppt = (D + kThreads - 1) / kThreads;
+      int p = tid * ppt;
+      const int pend = p + ppt < D ? p + ppt : D;
+      if (p < pend) {
+        int e = 0;
+        while (S.est_doff[e + 1] <= p) ++e;
+        U128 st = s0;
+        uint64_t out = 0;
+        int half = 0;
+        bool fresh = true;
+        for (; p < pend; ++p) {
+          uint32_t v;
+          if (h0 && p == 0) {
+            v = c.rng.uinteger;
+          } else {
+            if (fresh) {
+              const long long pp = p - (long long)h0;
+              st = pcg_jump(s0, (unsigned long long)(pp >> 1) + 1, S.jt);
+              out = pcg_output(st);
+              half = (int)(pp & 1);
+              fresh = false;
+            } else if (half == 0) {
+              half = 1;
+            } else {
+              st = add128(mul128(S.jt[0].a, st), S.jt[0].c);
+              out = pcg_output(st);
+              half = 0;
+            }
+            v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
+          }
+          while (S.est_doff[e + 1] <= p) ++e;
+          const int d = p - S.est_doff[e];
+          const uint32_t nunp = (uint32_t)S.est_nunp[e];
+          // Floyd draws bounded(j), j = n-k .. n-1, then the shuffle's bounded(i), i = k-1 .. 1
+          const uint32_t bound = d < Ssz ? nunp - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+          const uint32_t excl = bound + 1u;
+          const uint64_t mm = (uint64_t)v * excl;
+          const uint32_t left = (uint32_t)mm;
+          if (left < excl && left < (0xFFFFFFFFu - bound) % excl) S.rng_reject = 1;  // Lemire rejection
+          S.draws[p] = (uint32_t)(mm >> 32);
+        }
+      }
+    }
+    __syncthreads();
+    phase_mark(c, 6);
+    // 3. sample ratios
+    if (S.rng_reject) {  // a rejection shifts the stream: replay this batch sequentially
+      if (tid == 0) {
+        Pcg64 g = Pcg64::from(c.rng);
+        for (int e = 0; e < nb; ++e) S.est_ratio[e] = sample_ratio_seq(g, T, rq, P, S.est_rank[e]);
+        c.rng = g.to();
+      }
+    } else {
+      if (tid < nb) {
+        const int nunp = S.est_nunp[tid];
+        const int base = S.est_off[tid] + S.est_q[tid];
+        const long long mh = B * (long long)S.est_m[tid];  // exact utok = tok - B*m
+        double ratio = 0.0;
+        if (nunp > 0) {
+          long long usum = 0, tsum = 0;
+          if (nunp <= Ssz) {
+            for (int i = 0; i < nunp; ++i) {
+              const long long t = T.tok[base + i];
+              usum += t - mh;
+              tsum += t;
+            }
+          } else {
+            uint32_t idx[kMaxSample];
+            const int d0 = S.est_doff[tid];
+            for (int d = 0; d < Ssz; ++d) {  // Floyd's set; the shuffle only permutes it
+              const uint32_t j = (uint32_t)(nunp - Ssz + d);
+              const uint32_t v = S.draws[d0 + d];
+              bool found = false;
+              for (int x = 0; x < d; ++x) found |= idx[x] == v;
+              idx[d] = found ? j : v;
+            }
+            for (int d = 0; d < Ssz; ++d) {
+              const long long t = T.tok[base + (int)idx[d]];
+              usum += t - mh;
+              tsum += t;
+            }
+          }
+          ratio = __ddiv_rn((double)usum, (double)tsum);
+        }
+        S.est_ratio[tid] = ratio;
+      }
+      if (tid == 0 && D > 0) {  // advance the generator past the D values
+        const long long cnt = (long long)D - (long long)h0;
+        if (cnt <= 0) {
+          c.rng.has_uint32 = 0;
+        } else {
+          const U128 s1 = pcg_jump(s0, (unsigned long long)((cnt + 1) >> 1), S.jt);
+          c.rng.state_hi = s1.hi;
+          c.rng.state_lo = s1.lo;
+          if (cnt & 1) {
+            c.rng.has_uint32 = 1;
+            c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);
+          } else {
+            c.rng.has_uint32 = 0;
+          }
+        }
+      }
+    }
+    // running rows of each relQuery enter PEM as a prefilled summary (count,
+    // sum and max of remaining): they precede the unprefilled rows and fit
+    // the first segment (running <= mns)
+    for (int eb = warp; eb < nb; eb += kWarps) {
+      const int a = S.est_rank[eb];
+      const int ol = S.est_ol[eb];
+      PrefixSummary ps{0, 0, 0};
+      if (S.est_q[eb] > 0) {
+        long long rs = 0, cnt = 0, mx = 0;
+        for (int j = lane; j < c.n_run; j += 32)
+          if (c.run_rank[j] == a) {
+            const long long r = ol - c.run_gen[j];
+            rs += r;
+            cnt += 1;
+            mx = r > mx ? r : mx;
+          }
+        ps.n = (int)warp_sum(cnt);
+        ps.rsum = warp_sum(rs);
+        ps.rmax = (int)warp_max(mx);
+      }
+      if (lane == 0) S.est_ps[eb] = ps;
+    }
+    __syncthreads();
+    phase_mark(c, 7);
+    // 4. PEM
+    int items = 0;
+    for (int eb = 0; eb < nb; ++eb) items += S.est_nunp[eb];
+    if (T.seg_ok && items <= kItemBuf) {
+      SegBuf sb{S.seg.U, S.seg.UNP, S.seg.REM, S.seg.terms, S.seg.jcnt, S.seg.io, S.seg.jo};
+      EstItems ei{T.tok, S.est_off, S.est_q, S.est_nunp, S.est_ol, S.est_ratio};
+      seg_pem_batch(ei, nb, S.est_ps, pm, sb, S.segsh, PrioOut{rq.prio, S.est_rank});
+    } else {
+      for (int eb = warp; eb < nb; eb += kWarps) {
+        UnprefItems it{T.tok, S.est_off[eb] + S.est_q[eb], S.est_ol[eb], S.est_ratio[eb]};
+        const double v = warp_pem(it, S.est_nunp[eb], S.est_ps[eb], pm);
+        if (lane == 0) rq.prio[S.est_rank[eb]] = v;
+      }
+      __syncthreads();
+    }
+    phase_mark(c, 8);
+  }
+  // starvation override (priority.py:318-339): wholly waiting = no prefilled row = q == 0
+  if (isfinite(cfg.tau)) {
+    for (int a = tid; a < c.n_admitted; a += kThreads) {
+      const int size = rq.off[a + 1] - rq.off[a];
+      if (rq.q[a] == 0 && size > 0) {
+        const double uw = __ddiv_rn(__dsub_rn(c.clock, rq.arrival[a]), (double)size);
+        if (uw > cfg.tau) rq.prio[a] = 0.0;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace rsd

@@ -1,0 +1,214 @@
+// engine_state.cuh -- device data layout of the scheduler.
+//
+// Per trace, in HBM (structure of arrays, indexed by admission rank -- the
+// order relsim's DPU visits live relQueries, engine.py:211-213, 254, 279):
+//   relQuery table  arrival, row offsets, output_limit, chain blocks, rel_id
+//                   order, priority, prefilled prefix q, done/running counts,
+//                   prefix-cache chain state (m, c0, ntails)
+//   request rows    tok, out (EOS point), generated, completion iteration
+//   prefix cache    FIFO of resident private tails (insertion order)
+//   control block   clock, iteration, kv, queues, RNG, cache counters
+// During a launch the control block and, when it fits, the whole relQuery
+// table live in shared memory (RqView points at either copy).
+#pragma once
+#include <stdint.h>
+
+#include "../../include/relserve.h"
+#include "block.cuh"
+#include "pcg64.cuh"
+#include "pem.cuh"
+#include "seg_pem.cuh"
+#include "warp_pem.cuh"
+
+namespace rsd {
+
+constexpr int kMaxRun = 1024;   // device limit on max_num_seqs
+constexpr int kMaxAct = 1024;   // partially-prefilled live relQueries
+constexpr int kMaxCC = 256;     // tail-less resident chains
+constexpr int kWin = 768;       // FIFO window of the batched prefill eviction
+constexpr int kEstBatch = 128;  // relQueries re-estimated per DPU batch
+constexpr int kDrawBuf = 4096;  // numpy next32 draws staged per DPU batch
+constexpr int kItemBuf = 2048;  // PEM items staged per segment-parallel batch
+constexpr int kPhases = 16;
+
+struct FifoEnt {
+  unsigned long long t0;  // touch time of the tail's first block
+  int rank;               // owning relQuery
+  int tres;               // resident blocks of the tail
+};
+
+struct CcEnt {
+  unsigned long long key;  // touch time of the chain's last resident block
+  int rank;
+  int m;                   // resident chain blocks
+};
+
+// Persistent per-trace control block (global between launches, shared during one).
+struct alignas(16) Ctl {
+  double clock;
+  long long iteration;
+  long long kv;
+  long long hit, miss;
+  unsigned long long tclock;  // prefix-cache touch clock (prefix_cache.py:65-68)
+  long long count;            // resident blocks
+  long long n_log;
+  long long fifo_head, fifo_tail;
+  int n_admitted, live;
+  int n_run, n_act;
+  int status, error_detail;
+  int cc_n, n_rrq;
+  rs_pcg64_state rng;
+  long long phase[kPhases];  // clock64 cycles per phase (+ scratch timestamp in the last slot)
+  // running list (engine.py:205), in execution order, with the row state decode needs
+  int run_row[kMaxRun];
+  int run_rank[kMaxRun];
+  int run_gen[kMaxRun];
+  int run_out[kMaxRun];
+  int run_kv[kMaxRun];   // tok + output_limit reserved by the row
+  int act[kMaxAct];      // partially prefilled live relQueries, by rank
+  int rrq[kMaxRun];      // relQueries with running rows (distinct)
+  CcEnt cc[kMaxCC];
+};
+static_assert(sizeof(Ctl) % 16 == 0, "Ctl is copied as int4");
+
+// relQuery table view (shared or global memory).
+struct RqView {
+  double* prio;
+  double* arrival;
+  unsigned long long* c0;
+  int* off;  // [R+1]
+  int* q;
+  int* m;
+  int* ntails;
+  int* nrun;
+  int* ndone;
+  int* ol;
+  int* chain;
+  int* relrank;  // rank of the relQuery's rel_id among all rel_ids (tie order)
+  int* scr_cnt;
+  int* scr_last;
+};
+
+// bytes of the relQuery table for R relQueries (16-byte aligned sections)
+__host__ __device__ inline size_t rq_bytes(int R) {
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  return 3 * al(8 * (size_t)R) + al(4 * ((size_t)R + 1)) + 10 * al(4 * (size_t)R);
+}
+
+__host__ __device__ inline RqView rq_carve(void* base, int R) {
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  char* p = (char*)base;
+  RqView v;
+  v.prio = (double*)p;
+  p += al(8 * (size_t)R);
+  v.arrival = (double*)p;
+  p += al(8 * (size_t)R);
+  v.c0 = (unsigned long long*)p;
+  p += al(8 * (size_t)R);
+  v.off = (int*)p;
+  p += al(4 * ((size_t)R + 1));
+  int** ints[10] = {&v.q, &v.m, &v.ntails, &v.nrun, &v.ndone, &v.ol, &v.chain, &v.relrank, &v.scr_cnt, &v.scr_last};
+  for (int i = 0; i < 10; ++i) {
+    *ints[i] = (int*)p;
+    p += al(4 * (size_t)R);
+  }
+  return v;
+}
+
+struct TraceDev {
+  int R, N, max_size, seg_ok;  // seg_ok: mns * max(tok) <= cap (PEM segments close by count only)
+  int rq_in_smem, pad0;
+  void* rq_global;             // relQuery table (rq_carve layout)
+  const int* tok;              // [N] rank-ordered rows
+  const int* out;
+  int* gen;
+  int* comp;
+  double* fps;
+  double* lpe;
+  double* lde;
+  FifoEnt* fifo;
+  long long fifo_cap;
+  const JumpEntry* jump;  // PCG64 jump-ahead table of this trace's DPU generator
+  rs_iter_record* log;
+  long long log_cap;
+  Ctl* ctl;
+};
+
+struct Params {
+  const TraceDev* traces;
+  rs_config cfg;
+  rs_cost_model world;
+  rs_cost_model pol;
+  int use_dpu;
+  int force;  // 0 none, 1 prefill (relserve-pp), 2 decode (relserve-dp)
+  int prefill_first;
+  int pad;
+  long long max_iters;
+};
+
+struct Shared {
+  Ctl c;
+  RqView rq;
+  ArgminSmem am;
+  ScanSmem scan;
+  SegShared segsh;
+  JumpEntry jt[kJumpBits];
+  int go;
+  int new_lo, new_hi;
+  int head, W, taken, J;
+  long long utok_sum;
+  double m_plus, m_minus;
+  int dmin_slot, n_est;
+  int n_dist, act_dirty, rrq_dirty;
+  int sorted_dist[kMaxRun];
+  int cand_tok[kMaxRun];  // staged candidate prefill rows (tok, out)
+  int cand_out[kMaxRun];
+  // DPU batch
+  int est_rank[kEstBatch], est_off[kEstBatch], est_q[kEstBatch], est_nunp[kEstBatch];
+  int est_ol[kEstBatch], est_m[kEstBatch], est_doff[kEstBatch + 1];
+  double est_ratio[kEstBatch];
+  PrefixSummary est_ps[kEstBatch];
+  int rng_reject;
+  // batched prefill eviction
+  int fp_bad, fp_popped, fp_par, fp_cut;
+  long long fp_rem;
+  unsigned long long fp_c0_last;
+  union {
+    unsigned int draws[kDrawBuf];
+    struct {
+      long long U[kItemBuf];
+      double terms[2 * kItemBuf + kEstBatch];
+      int UNP[kItemBuf];
+      int REM[kItemBuf];
+      int jcnt[kItemBuf + kEstBatch];
+      int io[kEstBatch + 1];
+      int jo[kEstBatch + 1];
+    } seg;
+    struct {
+      unsigned long long t0[kWin];
+      unsigned long long c0[kWin];
+      int rank[kWin];
+      int tres[kWin];
+      int mm[kWin];
+      int last[kWin];  // 1 if this is the rank's last resident tail
+    } win;
+  };
+  // relQuery table follows (dynamic shared memory) when rq_in_smem
+};
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return (unsigned long long)__double_as_longlong(x);
+}
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7FF8000000000000LL); }
+
+// thread 0 accumulates the cycles since the previous mark into phase k
+__device__ __forceinline__ void phase_mark(Ctl& c, int k) {
+  if (threadIdx.x == 0) {
+    const long long now = clock64();
+    c.phase[k] += now - c.phase[kPhases - 1];
+    c.phase[kPhases - 1] = now;
+  }
+}
+
+}  // namespace rsd

@@ -108,3 +108,70 @@ __device__ __forceinline__ void choice_floyd(Pcg64& g, uint32_t n, uint32_t k, u
 }
 
 }  // namespace rsd
+
+namespace rsd {
+
+// ---------------------------------------------------------------------------
+// Jump-ahead: s_{t+n} = A^n s_t + C_n (mod 2^128).  tab[i] = (A^(2^i), C_(2^i)).
+// Lets every thread start at its own position of the numpy stream, so the
+// draws of many Generator.choice calls are produced in parallel and then
+// checked for Lemire rejections (which would shift the stream; the caller
+// falls back to the sequential replay when one occurs).
+// ---------------------------------------------------------------------------
+struct U128 {
+  uint64_t hi, lo;
+};
+
+struct JumpEntry {
+  U128 a, c;
+};
+
+constexpr int kJumpBits = 32;
+
+__host__ __device__ __forceinline__ U128 mul128(U128 x, U128 y) {
+  U128 r;
+#ifdef __CUDA_ARCH__
+  r.lo = x.lo * y.lo;
+  r.hi = __umul64hi(x.lo, y.lo) + x.lo * y.hi + x.hi * y.lo;
+#else
+  unsigned __int128 p = (unsigned __int128)x.lo * y.lo;
+  r.lo = (uint64_t)p;
+  r.hi = (uint64_t)(p >> 64) + x.lo * y.hi + x.hi * y.lo;
+#endif
+  return r;
+}
+
+__host__ __device__ __forceinline__ U128 add128(U128 x, U128 y) {
+  U128 r;
+  r.lo = x.lo + y.lo;
+  r.hi = x.hi + y.hi + (r.lo < x.lo ? 1ULL : 0ULL);
+  return r;
+}
+
+// tab[i] for i < kJumpBits, for a generator with increment inc.
+inline void pcg_jump_table(const rs_pcg64_state& st, JumpEntry* tab) {
+  U128 a{PCG_MULT_HI, PCG_MULT_LO};
+  U128 c{st.inc_hi, st.inc_lo};
+  for (int i = 0; i < kJumpBits; ++i) {
+    tab[i].a = a;
+    tab[i].c = c;
+    // (a, c) o (a, c): x -> a(ax + c) + c = a^2 x + (a + 1) c
+    U128 one{0, 1};
+    c = mul128(add128(a, one), c);
+    a = mul128(a, a);
+  }
+}
+
+__device__ __forceinline__ U128 pcg_jump(U128 s, unsigned long long n, const JumpEntry* tab) {
+  for (int i = 0; n; ++i, n >>= 1)
+    if (n & 1ULL) s = add128(mul128(tab[i].a, s), tab[i].c);
+  return s;
+}
+
+__device__ __forceinline__ uint64_t pcg_output(U128 s) {
+  const uint64_t x = s.hi ^ s.lo;
+  const unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+}  // namespace rsd
