@@ -173,19 +173,23 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   long long cT = 0, cTok = 0;
 #pragma unroll
   for (int s = 0; s < kMaxRun / kThreads; ++s) {
-    const int i = s * kThreads + tid;
-    long long tk = 0;
     Tv[s] = 0;
-    if (i < n) {
-      tk = tokv[i];
-      Tv[s] = tk / B - Pc;
-      if (Tv[s] <= 0) S.fp_bad = 1;
+    inclT[s] = 0;
+    if (s * kThreads < n) {
+      const int i = s * kThreads + tid;
+      int tk = 0, tl = 0;
+      if (i < n) {
+        tk = tokv[i];
+        tl = (int)(tk / B) - Pc;
+        if (tl <= 0) S.fp_bad = 1;
+      }
+      int v[2] = {tl, tk}, tot[2];
+      block_scan32<2>(v, S.s32, tot);
+      Tv[s] = tl;
+      inclT[s] = cT + v[0];
+      cT += tot[0];
+      cTok += tot[1];
     }
-    long long v[2] = {Tv[s], tk}, tot[2];
-    block_incl_scan<2>(v, S.scan, tot);
-    inclT[s] = cT + v[0];
-    cT += tot[0];
-    cTok += tot[1];
   }
   const long long newn = (long long)(Pc - m0) + cT;
   const long long E = count0 + newn > C ? count0 + newn - C : 0;
@@ -243,13 +247,12 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   bool par = S.fp_par;
   if (par && E > 0) {
     long long carry = 0;
-    long long cut_excl = 0;
     for (int base = 0; base < Wn; base += kThreads) {
       const int j = base + tid;
-      long long bj = 0;
+      int bj = 0;
       if (j < Wn) bj = S.win.tres[j] + (S.win.last[j] ? S.win.mm[j] : 0);
-      long long v[1] = {bj}, tot[1];
-      block_incl_scan<1>(v, S.scan, tot);
+      int v[1] = {bj}, tot[1];
+      block_scan32<1>(v, S.s32, tot);
       if (j < Wn && carry + v[0] >= E && carry + v[0] - bj < E) {  // the unique cut unit
         S.fp_cut = j;
         S.fp_rem = E - (carry + v[0] - bj);

@@ -114,8 +114,8 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
   if (tid == 0) S.n_est = n_est;
   for (int b0 = 0; b0 < n_est; b0 += batch) {
     const int nb = n_est - b0 < batch ? n_est - b0 : batch;
-    // 1. metadata and draw offsets
-    long long dcount = 0;
+    // 1. metadata; draw, item and PEM-segment offsets in one block scan
+    int dcount = 0, ni = 0, nj = 0;
     if (tid < nb) {
       const int e = b0 + tid;
       const int a = e < n_act ? c.act[e] : S.new_lo + (e - n_act);
@@ -129,17 +129,46 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
       S.est_ol[tid] = rq.ol[a];
       S.est_m[tid] = rq.m[a];
       dcount = size - q > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
+      ni = size - q;
+      const long long tot = (long long)ni + rq.nrun[a];  // running rows enter PEM as a prefilled summary
+      nj = tot > 0 ? (int)((tot + pm.mns - 1) / pm.mns) : 0;
     }
     {
-      long long v[1] = {dcount}, tot[1];
-      block_incl_scan<1>(v, S.scan, tot);
-      if (tid < nb) S.est_doff[tid] = (int)(v[0] - dcount);
+      int v[3] = {dcount, ni, nj}, tot[3];
+      block_scan32<3>(v, S.s32, tot);
+      if (tid < nb) {
+        S.est_doff[tid] = v[0] - dcount;
+        S.est_io[tid] = v[1] - ni;
+        S.est_jo[tid] = v[2] - nj;
+      }
       if (tid == 0) {
-        S.est_doff[nb] = (int)tot[0];
+        S.est_doff[nb] = tot[0];
+        S.est_io[nb] = tot[1];
+        S.est_jo[nb] = tot[2];
         S.rng_reject = 0;
       }
     }
     __syncthreads();
+    const int NI = S.est_io[nb];
+    const bool seg = T.seg_ok && NI <= kItemBuf;
+    // issue the PEM items' tok loads now; they land while the RNG runs
+    constexpr int kPer = kItemBuf / kThreads;
+    int tokr[kPer];
+    int item_e[kPer];
+    if (seg) {
+      int e = 0;
+#pragma unroll
+      for (int s = 0; s < kPer; ++s) {
+        const int x = s * kThreads + tid;
+        tokr[s] = 0;
+        item_e[s] = 0;
+        if (x < NI) {
+          while (S.est_io[e + 1] <= x) ++e;
+          item_e[s] = e;
+          tokr[s] = T.tok[S.est_off[e] + S.est_q[e] + (x - S.est_io[e])];
+        }
+      }
+    }
     phase_mark(c, 5);
     // 2. numpy's next32 stream, position p -> bounded draw, in parallel
     const int D = S.est_doff[nb];
@@ -212,10 +241,33 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
               usum += t - mh;
               tsum += t;
             }
+          } else if (Ssz <= 16) {  // Floyd's set in registers; the shuffle only permutes it
+            const int d0 = S.est_doff[tid];
+            uint32_t idx[16];
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+              if (d < Ssz) {
+                const uint32_t j = (uint32_t)(nunp - Ssz + d);
+                const uint32_t v = S.draws[d0 + d];
+                bool found = false;
+#pragma unroll
+                for (int x = 0; x < 16; ++x) found |= (x < d) && idx[x] == v;
+                idx[d] = found ? j : v;
+              }
+            }
+            long long tv[16];
+#pragma unroll
+            for (int d = 0; d < 16; ++d) tv[d] = d < Ssz ? T.tok[base + (int)idx[d]] : 0;
+#pragma unroll
+            for (int d = 0; d < 16; ++d)
+              if (d < Ssz) {
+                usum += tv[d] - mh;
+                tsum += tv[d];
+              }
           } else {
             uint32_t idx[kMaxSample];
             const int d0 = S.est_doff[tid];
-            for (int d = 0; d < Ssz; ++d) {  // Floyd's set; the shuffle only permutes it
+            for (int d = 0; d < Ssz; ++d) {
               const uint32_t j = (uint32_t)(nunp - Ssz + d);
               const uint32_t v = S.draws[d0 + d];
               bool found = false;
@@ -274,12 +326,31 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
     __syncthreads();
     phase_mark(c, 7);
     // 4. PEM
-    int items = 0;
-    for (int eb = 0; eb < nb; ++eb) items += S.est_nunp[eb];
-    if (T.seg_ok && items <= kItemBuf) {
-      SegBuf sb{S.seg.U, S.seg.UNP, S.seg.REM, S.seg.terms, S.seg.jcnt, S.seg.io, S.seg.jo};
-      EstItems ei{T.tok, S.est_off, S.est_q, S.est_nunp, S.est_ol, S.est_ratio};
-      seg_pem_batch(ei, nb, S.est_ps, pm, sb, S.segsh, PrioOut{rq.prio, S.est_rank});
+    if (seg) {
+      SegBuf sb{S.seg.U, S.seg.UNP, S.seg.REM, S.seg.terms, S.seg.jcnt, S.est_io, S.est_jo};
+      // each thread materialises exactly the items whose tok it loaded
+      long long carryU = 0, carryN = 0;
+#pragma unroll
+      for (int s = 0; s < kPer; ++s) {
+        const int x = s * kThreads + tid;
+        if (s * kThreads < NI) {
+          int u = 0;
+          if (x < NI) {
+            u = (int)utok_approx(tokr[s], S.est_ratio[item_e[s]]);
+            S.seg.REM[x] = S.est_ol[item_e[s]];
+          }
+          int v[2] = {u, x < NI ? 1 : 0}, tot[2];
+          block_scan32<2>(v, S.s32, tot);
+          if (x < NI) {
+            S.seg.U[x] = carryU + v[0];
+            S.seg.UNP[x] = (int)(carryN + v[1]);
+          }
+          carryU += tot[0];
+          carryN += tot[1];
+        }
+      }
+      __syncthreads();
+      seg_jobs_and_sum(nb, S.est_ps, pm, sb, PrioOut{rq.prio, S.est_rank});
     } else {
       for (int eb = warp; eb < nb; eb += kWarps) {
         UnprefItems it{T.tok, S.est_off[eb] + S.est_q[eb], S.est_ol[eb], S.est_ratio[eb]};

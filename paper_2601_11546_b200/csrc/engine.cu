@@ -81,57 +81,78 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   phase_mark(c, 1);
 
   // ---- C: waiting head = argmin (prio, rank) over relQueries with pending
-  // rows, and W = len(waiting)
+  // rows, and W = len(waiting); one fused block reduction
+  int head_l;
   {
     unsigned long long key = ~0ULL;
-    long long idx = 0x7FFFFFFFFFFFFFFFLL;
-    long long w = 0;
+    int idx = 0x7FFFFFFF;
+    int w = 0;
     for (int a = tid; a < c.n_admitted; a += kThreads) {
       if (rq.q[a] < rq.off[a + 1] - rq.off[a]) {
         ++w;
-        argmin_merge(key, idx, dbits(rq.prio[a]), a);
+        const unsigned long long k = dbits(rq.prio[a]);
+        if (k < key) {  // ranks visited in increasing order: strict < keeps the smallest rank
+          key = k;
+          idx = a;
+        }
       }
     }
-    const long long W = block_sum(w, S.scan);
-    block_argmin(key, idx, S.am);
+    block_count_argmin(w, key, idx, S.red);  // result is block-uniform in registers
+    head_l = w > 0 ? idx : -1;
     if (tid == 0) {
-      S.W = (int)W;
-      S.head = W > 0 ? (int)idx : -1;
+      S.W = w;
+      S.head = head_l;  // read by other threads only after later barriers
     }
   }
   phase_mark(c, 2);
 
   // ---- D: candidates (engine.py:285-308)
   {
-    // decode candidate = running list; m+ and the first running row attaining it
-    unsigned long long key = ~0ULL;
-    long long idx = 0x7FFFFFFFFFFFFFFFLL;
-    for (int j = tid; j < c.n_run; j += kThreads) argmin_merge(key, idx, dbits(rq.prio[c.run_rank[j]]), j);
-    block_argmin(key, idx, S.am);
+    // decode candidate = running list.  m+ = min over the distinct running
+    // relQueries (rrq); the first running row attaining it only matters when
+    // two distinct relQueries tie on m+.
     if (tid == 0) {
-      S.dmin_slot = c.n_run > 0 ? (int)idx : -1;
-      S.m_plus = c.n_run > 0 ? rq.prio[c.run_rank[idx]] : qnan();
+      double best = 0.0;
+      int brank = -1, nties = 0;
+      for (int i = 0; i < c.n_rrq; ++i) {
+        const double p = rq.prio[c.rrq[i]];
+        if (brank < 0 || p < best) {
+          best = p;
+          brank = c.rrq[i];
+          nties = 1;
+        } else if (p == best) {
+          ++nties;
+        }
+      }
+      if (nties > 1) {
+        for (int j = 0; j < c.n_run; ++j)
+          if (rq.prio[c.run_rank[j]] == best) {
+            brank = c.run_rank[j];
+            break;
+          }
+      }
+      S.dmin_slot = brank;  // rank of the first running row with the minimum priority
+      S.m_plus = c.n_run > 0 ? best : qnan();
+      S.first_bad = 0x7FFFFFFF;
     }
     phase_mark(c, 11);
     // prefill candidate: leading run of the head's pending rows (arranger.py:80-112)
-    const int h = S.head;
-    int J = 0, base_row = 0;
-    long long mh = 0, olh = 0;
+    const int h = head_l;
+    int J = 0, base_row = 0, mh = 0, olh = 0;
     if (h >= 0) {
       const int q = rq.q[h];
       base_row = rq.off[h] + q;
       const int pend = rq.off[h + 1] - base_row;
       const long long room = cfg.max_num_seqs - c.n_run;
       J = room <= 0 ? 0 : (int)(pend < room ? pend : room);
-      mh = cfg.block_size * (long long)rq.m[h];
+      mh = (int)(cfg.block_size * (long long)rq.m[h]);
       olh = rq.ol[h];
     }
     const long long headroom = cfg.cap - c.kv;
-    long long cu = 0, ck = 0;
-    long long first_bad = J;
+    int cu = 0, ck = 0;
     for (int base = 0; base < J; base += kThreads) {
       const int j = base + tid;
-      long long v[2] = {0, 0};
+      int v[2] = {0, 0};
       if (j < J) {
         const int t = T.tok[base_row + j];
         S.cand_tok[j] = t;
@@ -139,32 +160,30 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         v[0] = t - mh;   // exact utok (match_uncached, refresh=False)
         v[1] = t + olh;  // kv need
       }
-      long long tot[2];
-      block_incl_scan<2>(v, S.scan, tot);
-      long long bad = 0x7FFFFFFFFFFFFFFFLL;
+      int tot[2];
+      block_scan32<2>(v, S.s32, tot);
+      bool bad = false;
       if (j < J) {
-        const long long U = cu + v[0], K = ck + v[1];
-        if ((j > 0 && U > cfg.max_num_batched_tokens) || K > headroom) bad = j;
+        const int U = cu + v[0], K = ck + v[1];
+        S.cand_u[j] = U;
+        bad = (j > 0 && U > cfg.max_num_batched_tokens) || K > headroom;
       }
-      unsigned long long kk = (unsigned long long)bad;
-      long long ii = bad;
-      block_argmin(kk, ii, S.am);
-      if ((long long)kk < first_bad) first_bad = (long long)kk;
+      const unsigned m = __ballot_sync(kFull, bad);
+      if (m && (tid & 31) == 0) atomicMin(&S.first_bad, base + (tid & ~31) + __ffs(m) - 1);
       cu += tot[0];
       ck += tot[1];
-      if (first_bad < J) break;
+      __syncthreads();
+      if (S.first_bad < J) break;
     }
-    if (tid == 0) S.taken = (int)first_bad;
+    if (tid == 0) {
+      const int taken = S.first_bad < J ? S.first_bad : J;
+      S.taken = taken;
+      S.cand_mh = mh;
+      S.utok_sum = taken > 0 ? S.cand_u[taken - 1] : 0;
+      S.m_minus = taken > 0 ? rq.prio[h] : qnan();
+    }
     __syncthreads();
     phase_mark(c, 12);
-    long long us = 0;
-    for (int j = tid; j < S.taken; j += kThreads) us += S.cand_tok[j] - mh;
-    us = block_sum(us, S.scan);
-    if (tid == 0) {
-      S.utok_sum = us;
-      S.m_minus = S.taken > 0 ? rq.prio[h] : qnan();
-    }
-    __syncthreads();
   }
 
   // ---- E: decision (engine.py:387-433, arranger.py:115-179)
@@ -223,7 +242,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       } else if (!has_p) {
         action = RS_ACTION_DECODE;
         kase = RS_CASE_FORCED;
-      } else if (c.run_rank[S.dmin_slot] == S.head) {
+      } else if (S.dmin_slot == S.head) {
         action = RS_ACTION_PREFILL;
         kase = RS_CASE_INTERNAL;
       } else if (S.m_plus > S.m_minus) {
@@ -239,7 +258,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         else action = (ddt < 0) ? RS_ACTION_PREFILL : RS_ACTION_DECODE;
       }
     }
-    S.go = action;  // reuse as the action slot
+    S.action = action;
     if (cfg.log_decisions && T.log_cap > 0) {
       rs_iter_record& r = T.log[c.n_log % T.log_cap];
       r.iteration = c.iteration;
@@ -261,7 +280,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
   }
   __syncthreads();
-  const int action = S.go;
+  const int action = S.action;
   phase_mark(c, 3);
 
   // ---- F: execute
@@ -320,19 +339,16 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       }
       S.go = ok && c.status == RS_RUNNING;
     }
-    // running list append + kv reservation (engine.py:326-329)
-    long long kv = 0;
+    // running list append + kv reservation (engine.py:326-329): sum of
+    // (tok + output_limit) = candidate kv prefix at n-1
     for (int i = tid; i < n; i += kThreads) {
-      const int kvw = S.cand_tok[i] + ol;
       c.run_row[n_run0 + i] = row0 + i;
       c.run_rank[n_run0 + i] = h;
       c.run_gen[n_run0 + i] = 0;
       c.run_out[n_run0 + i] = S.cand_out[i];
-      c.run_kv[n_run0 + i] = kvw;
-      kv += kvw;
+      c.run_kv[n_run0 + i] = S.cand_tok[i] + ol;
     }
-    kv = block_sum(kv, S.scan);
-    if (tid == 0) c.kv += kv;
+    if (tid == 0) c.kv += (long long)S.cand_u[n - 1] + (long long)n * (S.cand_mh + ol);
     __syncthreads();
     phase_mark(c, 10);
     if (!S.go) return false;
@@ -344,7 +360,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     __syncthreads();
     const double clk = __dadd_rn(c.clock, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d));
-    long long kv_free = 0;
+    int kv_free = 0;
     int keep[kMaxRun / kThreads], nrow[kMaxRun / kThreads], nrank[kMaxRun / kThreads];
     int ngen[kMaxRun / kThreads], nout[kMaxRun / kThreads], nkv[kMaxRun / kThreads];
 #pragma unroll
@@ -375,26 +391,32 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         }
       }
     }
-    kv_free = block_sum(kv_free, S.scan);  // (syncs: all reads of the old list are done)
+    // stable compaction of the running list + freed kv, one fused scan per
+    // tile (the scan's first barrier orders all reads of the old list)
     int cbase = 0;
+    long long kv_total = 0;
 #pragma unroll
     for (int s = 0; s < kMaxRun / kThreads; ++s) {
-      long long v[1] = {keep[s]}, tot[1];
-      block_incl_scan<1>(v, S.scan, tot);
-      if (keep[s]) {
-        const int d = cbase + (int)v[0] - 1;
-        c.run_row[d] = nrow[s];
-        c.run_rank[d] = nrank[s];
-        c.run_gen[d] = ngen[s];
-        c.run_out[d] = nout[s];
-        c.run_kv[d] = nkv[s];
+      if (s * kThreads < n) {
+        int v[2] = {keep[s], (int)kv_free}, tot[2];
+        kv_free = 0;
+        block_scan32<2>(v, S.s32, tot);
+        if (keep[s]) {
+          const int d = cbase + v[0] - 1;
+          c.run_row[d] = nrow[s];
+          c.run_rank[d] = nrank[s];
+          c.run_gen[d] = ngen[s];
+          c.run_out[d] = nout[s];
+          c.run_kv[d] = nkv[s];
+        }
+        cbase += tot[0];
+        kv_total += tot[1];
       }
-      cbase += (int)tot[0];
     }
     __syncthreads();
     if (tid == 0) {
       c.n_run = cbase;
-      c.kv -= kv_free;
+      c.kv -= kv_total;
       c.clock = clk;
       if (cfg.log_decisions && T.log_cap > 0) T.log[c.n_log % T.log_cap].batch_n = n;
       if (S.rrq_dirty) {
@@ -450,8 +472,11 @@ __device__ __forceinline__ void copy16(void* dst, const void* src, size_t bytes)
 
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ TraceDev Tsm;  // the trace's pointers, read on every access
   Shared& S = *reinterpret_cast<Shared*>(smem_raw);
-  const TraceDev& T = P.traces[blockIdx.x];
+  if (threadIdx.x == 0) Tsm = P.traces[blockIdx.x];
+  __syncthreads();
+  const TraceDev& T = Tsm;
   copy16(&S.c, T.ctl, sizeof(Ctl));
   for (int i = threadIdx.x; i < kJumpBits; i += kThreads) S.jt[i] = T.jump[i];
   const size_t rqb = rq_bytes(T.R);
@@ -699,6 +724,8 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_pc
                  (long long)(r - lo), (long long)tok[k] + ol[a], (long long)cfg->cap);
         return fail(RS_EINFEASIBLE, msg);
       }
+      if ((long long)tok[k] + ol[a] >= (1LL << 20))
+        return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
       const long long nb = tok[k] / cfg->block_size;
       if (nb < chain[a]) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
       if (nb > max_nb) max_nb = nb;

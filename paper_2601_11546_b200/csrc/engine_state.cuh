@@ -151,9 +151,11 @@ struct Shared {
   RqView rq;
   ArgminSmem am;
   ScanSmem scan;
+  Scan32Smem s32;
+  RedSmem red;
   SegShared segsh;
   JumpEntry jt[kJumpBits];
-  int go;
+  int go, action;
   int new_lo, new_hi;
   int head, W, taken, J;
   long long utok_sum;
@@ -163,9 +165,12 @@ struct Shared {
   int sorted_dist[kMaxRun];
   int cand_tok[kMaxRun];  // staged candidate prefill rows (tok, out)
   int cand_out[kMaxRun];
+  int cand_u[kMaxRun];     // inclusive utok prefix of the candidate rows
+  int first_bad, cand_mh;
   // DPU batch
   int est_rank[kEstBatch], est_off[kEstBatch], est_q[kEstBatch], est_nunp[kEstBatch];
   int est_ol[kEstBatch], est_m[kEstBatch], est_doff[kEstBatch + 1];
+  int est_io[kEstBatch + 1], est_jo[kEstBatch + 1];  // PEM item / job offsets
   double est_ratio[kEstBatch];
   PrefixSummary est_ps[kEstBatch];
   int rng_reject;
@@ -181,8 +186,6 @@ struct Shared {
       int UNP[kItemBuf];
       int REM[kItemBuf];
       int jcnt[kItemBuf + kEstBatch];
-      int io[kEstBatch + 1];
-      int jo[kEstBatch + 1];
     } seg;
     struct {
       unsigned long long t0[kWin];

@@ -34,59 +34,61 @@ struct SegShared {
   ScanSmem scan;
 };
 
-// F::count(e), F::item(e, i, u, rem, pre).  ps[e] = prefilled summary of
-// remainder e.  Writes the PEM of remainder e to out(e, value) via G.
-// NI = sum of counts must fit the buffers (checked by the caller).
-template <class F, class G>
-__device__ void seg_pem_batch(const F& f, int nb, const PrefixSummary* ps, const PemModel& m, SegBuf b,
-                              SegShared& sh, const G& out) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // item and job offsets
-  {
-    long long ni = 0, nj = 0;
-    if (tid < nb) {
-      ni = f.count(tid);
-      const long long tot = ni + ps[tid].n;
-      nj = tot > 0 ? (tot + m.mns - 1) / m.mns : 0;
+// Item / job offsets of a batch (all threads; tid < nb supplies count(tid)).
+template <class F>
+__device__ void seg_offsets(const F& f, int nb, const PrefixSummary* ps, const PemModel& m, SegBuf b,
+                            SegShared& sh) {
+  const int tid = threadIdx.x;
+  long long ni = 0, nj = 0;
+  if (tid < nb) {
+    ni = f.count(tid);
+    const long long tot = ni + ps[tid].n;
+    nj = tot > 0 ? (tot + m.mns - 1) / m.mns : 0;
+  }
+  long long v[2] = {ni, nj}, tot[2];
+  block_incl_scan<2>(v, sh.scan, tot);
+  if (tid < nb) {
+    b.io[tid] = (int)(v[0] - ni);
+    b.jo[tid] = (int)(v[1] - nj);
+  }
+  if (tid == 0) {
+    b.io[nb] = (int)tot[0];
+    b.jo[nb] = (int)tot[1];
+  }
+  __syncthreads();
+}
+
+// Materialise items: G(x, u, rem, pre) for item x of the concatenated batch;
+// one inclusive scan of utok and of the unprefilled count over the batch.
+template <class G>
+__device__ void seg_materialize(const G& g, int NI, SegBuf b, SegShared& sh) {
+  const int tid = threadIdx.x;
+  long long carryU = 0, carryN = 0;
+  for (int base = 0; base < NI; base += kThreads) {
+    const int x = base + tid;
+    long long u = 0;
+    int rem = 0, pre = 1;
+    if (x < NI) {
+      g(x, u, rem, pre);
+      b.REM[x] = rem;
     }
-    long long v[2] = {ni, nj}, tot[2];
+    long long v[2] = {u, (x < NI && !pre) ? 1LL : 0LL}, tot[2];
     block_incl_scan<2>(v, sh.scan, tot);
-    if (tid < nb) {
-      b.io[tid] = (int)(v[0] - ni);
-      b.jo[tid] = (int)(v[1] - nj);
+    if (x < NI) {
+      b.U[x] = carryU + v[0];
+      b.UNP[x] = (int)(carryN + v[1]);
     }
-    if (tid == 0) {
-      b.io[nb] = (int)tot[0];
-      b.jo[nb] = (int)tot[1];
-    }
+    carryU += tot[0];
+    carryN += tot[1];
   }
   __syncthreads();
-  const int NI = b.io[nb], J = b.jo[nb];
-  // materialise items; one inclusive scan over the concatenated remainders
-  {
-    int e = 0;
-    long long carryU = 0, carryN = 0;
-    for (int base = 0; base < NI; base += kThreads) {
-      const int x = base + tid;
-      long long u = 0;
-      int rem = 0, pre = 1;
-      if (x < NI) {
-        while (b.io[e + 1] <= x) ++e;
-        f.item(e, x - b.io[e], u, rem, pre);
-        b.REM[x] = rem;
-      }
-      long long v[2] = {u, (x < NI && !pre) ? 1LL : 0LL}, tot[2];
-      block_incl_scan<2>(v, sh.scan, tot);
-      if (x < NI) {
-        b.U[x] = carryU + v[0];
-        b.UNP[x] = (int)(carryN + v[1]);
-      }
-      carryU += tot[0];
-      carryN += tot[1];
-    }
-  }
-  __syncthreads();
-  // one warp per segment job
+}
+
+// Segment jobs (one warp each) and the ordered per-remainder sums.
+template <class G>
+__device__ void seg_jobs_and_sum(int nb, const PrefixSummary* ps, const PemModel& m, SegBuf b, const G& out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int J = b.jo[nb];
   for (int j = warp; j < J; j += kWarps) {
     int e = 0;
     while (b.jo[e + 1] <= j) ++e;
@@ -101,11 +103,12 @@ __device__ void seg_pem_batch(const F& f, int nb, const PrefixSummary* ps, const
     const int* UNP = b.UNP + b.io[e];
     const int g0 = b.io[e] + t0;
     const long long Ub = g0 > 0 ? b.U[g0 - 1] : 0, Nb = g0 > 0 ? b.UNP[g0 - 1] : 0;
-    // relative prefix sums inside the segment
     double* out_terms = b.terms + b.io[e] + b.jo[e] + k + t0;
     int nterm = 0;
     int bb = t0;
     while (bb < t1) {
+      // sub-batch [bb, nbk): closes before the first later item j with
+      // utok_j > 0 and utok(bb..j) > mnbt (priority.py:205-208)
       const long long before = bb > t0 ? U[bb - 1] - Ub : 0;
       const long long ub = U[bb] - Ub;
       const long long thr = ub - before > m.mnbt ? ub : before + m.mnbt;
@@ -146,21 +149,48 @@ __device__ void seg_pem_batch(const F& f, int nb, const PrefixSummary* ps, const
     }
   }
   __syncthreads();
-  // ordered sums
+  // ordered sums: segment by segment, terms in emission order
   if (tid < nb) {
     double total = 0.0;
-    const int n = b.io[tid + 1] - b.io[tid];
-    for (int k = 0; k < b.jo[tid + 1] - b.jo[tid]; ++k) {
+    const int nj = b.jo[tid + 1] - b.jo[tid];
+    for (int k = 0; k < nj; ++k) {
       const long long t0l = (long long)k * m.mns - ps[tid].n;
       const int t0 = t0l < 0 ? 0 : (int)t0l;
       const double* tt = b.terms + b.io[tid] + b.jo[tid] + k + t0;
-      const int c = b.jcnt[b.jo[tid] + k];
-      for (int i = 0; i < c; ++i) total = __dadd_rn(total, tt[i]);
+      const int cnt = b.jcnt[b.jo[tid] + k];
+      int i = 0;
+      for (; i + 4 <= cnt; i += 4) {  // independent loads, dependent adds
+        const double x0 = tt[i], x1 = tt[i + 1], x2 = tt[i + 2], x3 = tt[i + 3];
+        total = __dadd_rn(total, x0);
+        total = __dadd_rn(total, x1);
+        total = __dadd_rn(total, x2);
+        total = __dadd_rn(total, x3);
+      }
+      for (; i < cnt; ++i) total = __dadd_rn(total, tt[i]);
     }
-    (void)n;
     out(tid, total);
   }
   __syncthreads();
+}
+
+// F::count(e), F::item(e, i, u, rem, pre); the whole pipeline for one batch.
+template <class F, class G>
+__device__ void seg_pem_batch(const F& f, int nb, const PrefixSummary* ps, const PemModel& m, SegBuf b,
+                              SegShared& sh, const G& out) {
+  seg_offsets(f, nb, ps, m, b, sh);
+  const int NI = b.io[nb];
+  struct ByItem {
+    const F& f;
+    const int* io;
+    int nb;
+    __device__ void operator()(int x, long long& u, int& rem, int& pre) const {
+      int e = 0;
+      while (io[e + 1] <= x) ++e;
+      f.item(e, x - io[e], u, rem, pre);
+    }
+  };
+  seg_materialize(ByItem{f, b.io, nb}, NI, b, sh);
+  seg_jobs_and_sum(nb, ps, m, b, out);
 }
 
 }  // namespace rsd

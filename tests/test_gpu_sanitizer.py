@@ -1,0 +1,53 @@
+"""compute-sanitizer racecheck / memcheck over short device runs (SURVEY 5:
+race detection).  Skipped when compute-sanitizer is not on PATH."""
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+SCRIPT = r"""
+import sys; sys.path.insert(0, {root!r})
+from paper_2601_11546_b200 import *
+from paper_2601_11546_b200.engine import Engine
+for policy, tc, kw in [("sp", dict(num_relqueries=40, size_range=(1, 40), rate=10.0, seed=36), {{}}),
+                       ("relserve", dict(num_relqueries=30, size_range=(1, 60), rate=5.0, seed=3),
+                        dict(capacity_blocks=120, tau=0.2))]:
+    t = generate_trace(TraceConfig(**tc))
+    e = Engine(t, policy, world_preset("opt-13b-like"), EngineConfig(iteration_limit=60, **kw))
+    try:
+        e.run()
+    except SimulationAborted:
+        pass
+    e.close()
+print("ran")
+"""
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    return None
+
+
+@pytest.mark.parametrize("tool", ["racecheck", "memcheck"])
+def test_sanitizer_clean(tool, tmp_path):
+    cs = _sanitizer()
+    if cs is None:
+        pytest.skip("compute-sanitizer not available")
+    script = tmp_path / "run.py"
+    script.write_text(SCRIPT.format(root=str(ROOT)))
+    args = [cs, "--tool", tool, "--error-exitcode", "17"]
+    if tool == "racecheck":
+        args += ["--racecheck-report", "hazard"]
+    r = subprocess.run(args + [sys.executable, str(script)], capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert "ran" in out, out[-3000:]
+    assert r.returncode == 0, out[-3000:]
