@@ -42,8 +42,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "sched iters/sec @1M pending reqs"
-PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dpu_rng", "dpu_ratio_prefix",
-          "dpu_pem", "fp_evict_post", "prefill_post", "cand_decode", "cand_prefill", "fp_scan", "fp_stage")
+PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dpu_rng", "dpu_summaries",
+          "dpu_pem", "fp_evict_post", "prefill_post", "cand_decode", "cand_prefill", "fp_scan", "fp_stage",
+          "dpu_ratio", "p16", "p17", "p18", "p19", "p20", "p21", "p22")
 WINDOW_START = 5
 
 
@@ -52,12 +53,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--iters-per-step", type=int, default=2000)
+    ap.add_argument("--iters-per-step", type=int, default=250)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["2", "3"], default="2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=1500)
+    ap.add_argument("--cpu-iters", type=int, default=6000)
     return ap.parse_args()
 
 
@@ -354,7 +355,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return None
     trace, world, cfg, wname = workload(args.config, seed=0)
-    per_step = max(1, args.iters_per_step // 20)
+    per_step = max(1, args.iters_per_step)
     n = WINDOW_START + (args.warmup + args.steps) * per_step
     from dataclasses import replace
 

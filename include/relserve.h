@@ -135,7 +135,7 @@ typedef struct {
   /* device clock64() cycles per phase, summed over iterations: [0] admission,
      [1] priority update (DPU) remainder, [2] waiting order, [3] candidates +
      decision (ABA), [4] execution; finer marks [5..14] (see bench.py PHASES) */
-  int64_t phase_cycles[15];
+  int64_t phase_cycles[23];
 } rs_trace_status;
 
 typedef struct rs_engine rs_engine;

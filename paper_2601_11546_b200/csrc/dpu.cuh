@@ -91,6 +91,256 @@ __device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq
   return __ddiv_rn((double)usum, (double)tsum);
 }
 
+
+// Fast path for the common steady state (few re-estimated relQueries, PEM
+// segments closed by count only, mns <= 256, sample size <= 16): two block
+// barriers in total.
+//   * every warp derives the per-relQuery metadata and the draw / segment
+//     offsets itself (lane e = relQuery e, warp scans; no barrier);
+//   * warp 0 replays the numpy draws from jump-ahead (lane per position) and
+//     computes the sample ratios; the other warps build the running-row
+//     summaries;
+//   * one warp per PEM segment materialises its utok prefix, follows the
+//     sub-batch chain with ballots, and emits its terms;
+//   * lane e of warp 0 adds relQuery e's terms in the reference's order.
+// Returns false (nothing changed) when the preconditions do not hold.
+__device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const PemModel& pm) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const rs_config& cfg = P.cfg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_act = c.n_act;
+  const int n_est = n_act + (S.new_hi - S.new_lo);
+  const int Ssz = (int)cfg.sample_size;
+  if (n_est > kSmallEst || !T.seg_ok || pm.mns > kSmallMns || Ssz > 16) return false;
+  const int dper = 2 * Ssz - 1;
+  // per-warp metadata: lane e holds relQuery e
+  int a = 0, base = 0, nunp = 0, ol = 0, mcb = 0, L = 0, dcnt = 0, nj = 0;
+  if (lane < n_est) {
+    a = lane < n_act ? c.act[lane] : S.new_lo + (lane - n_act);
+    const int off = rq.off[a];
+    const int q = rq.q[a];
+    base = off + q;
+    nunp = rq.off[a + 1] - base;
+    ol = rq.ol[a];
+    mcb = rq.m[a];
+    L = rq.nrun[a];  // running rows = the live prefilled rows (prefilled summary)
+    dcnt = nunp > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
+    const long long tot = (long long)nunp + L;
+    nj = tot > 0 ? (int)((tot + pm.mns - 1) / pm.mns) : 0;
+  }
+  const int dincl = warp_incl_scan(dcnt), jincl = warp_incl_scan(nj);
+  const int doff = dincl - dcnt, jo = jincl - nj;
+  const int D = __shfl_sync(kFull, dincl, 31), J = __shfl_sync(kFull, jincl, 31);
+  if (J > kMaxJobs) return false;
+  if (tid == 0) S.n_est = n_est;
+  phase_mark(c, 5);
+  if (warp == 0) {
+    // numpy next32 stream positions [0, D) -> bounded draws
+    const unsigned h0 = c.rng.has_uint32;
+    const U128 s0{c.rng.state_hi, c.rng.state_lo};
+    bool rej = false;
+    if (lane < n_est) {  // owner lookup tables for the (divergent) position loop
+      S.est_doff[lane] = dcnt > 0 ? doff : 0x7FFFFFFF;
+      S.est_nunp[lane] = nunp;
+    }
+    __syncwarp();
+    for (int p = lane; p < D; p += 32) {
+      uint32_t v;
+      if (h0 && p == 0) {
+        v = c.rng.uinteger;
+      } else {
+        const long long pp = p - (long long)h0;
+        const uint64_t out = pcg_output(pcg_jump(s0, (unsigned long long)(pp >> 1) + 1, S.jt));
+        v = (pp & 1) ? (uint32_t)(out >> 32) : (uint32_t)out;
+      }
+      int e = 0;  // relQuery owning position p: the last one with a draw offset <= p
+      for (int x = 0; x < n_est; ++x)
+        if (S.est_doff[x] <= p) e = x;
+      const int d = p - S.est_doff[e];
+      const uint32_t ne = (uint32_t)S.est_nunp[e];
+      const uint32_t bound = d < Ssz ? ne - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+      const uint32_t excl = bound + 1u;
+      const uint64_t mm = (uint64_t)v * excl;
+      const uint32_t left = (uint32_t)mm;
+      if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;  // Lemire rejection
+      S.small.draws[p] = (uint32_t)(mm >> 32);
+    }
+    rej = __any_sync(kFull, rej);
+    __syncwarp();
+    phase_mark(c, 6);
+    if (rej) {  // replay sequentially: a rejection shifts every later draw
+      if (lane == 0) {
+        Pcg64 g = Pcg64::from(c.rng);
+        for (int e = 0; e < n_est; ++e) {
+          const int ae = e < n_act ? c.act[e] : S.new_lo + (e - n_act);
+          S.est_ratio[e] = sample_ratio_seq(g, T, rq, P, ae);
+        }
+        c.rng = g.to();
+      }
+    } else {
+      if (lane < n_est) {  // sample_cache_miss_ratio (prefix_cache.py:141-169)
+        const long long mh = cfg.block_size * (long long)mcb;  // exact utok = tok - B*m
+        double ratio = 0.0;
+        if (nunp > 0) {
+          long long usum = 0, tsum = 0;
+          if (nunp <= Ssz) {
+            for (int i = 0; i < nunp; ++i) {
+              const long long t = T.tok[base + i];
+              usum += t - mh;
+              tsum += t;
+            }
+          } else {
+            uint32_t idx[16];
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+              if (d < Ssz) {  // Floyd's set; the shuffle only permutes it
+                const uint32_t j = (uint32_t)(nunp - Ssz + d);
+                const uint32_t v = S.small.draws[doff + d];
+                bool found = false;
+#pragma unroll
+                for (int x = 0; x < 16; ++x) found |= (x < d) && idx[x] == v;
+                idx[d] = found ? j : v;
+              }
+            }
+            long long tv[16];
+#pragma unroll
+            for (int d = 0; d < 16; ++d) tv[d] = d < Ssz ? T.tok[base + (int)idx[d]] : 0;
+#pragma unroll
+            for (int d = 0; d < 16; ++d)
+              if (d < Ssz) {
+                usum += tv[d] - mh;
+                tsum += tv[d];
+              }
+          }
+          ratio = __ddiv_rn((double)usum, (double)tsum);
+        }
+        S.est_ratio[lane] = ratio;
+      }
+      __syncwarp();
+      phase_mark(c, 15);
+      if (lane == 0 && D > 0) {  // advance the generator past the D values
+        const long long cnt = (long long)D - (long long)h0;
+        if (cnt <= 0) {
+          c.rng.has_uint32 = 0;
+        } else {
+          const U128 s1 = pcg_jump(s0, (unsigned long long)((cnt + 1) >> 1), S.jt);
+          c.rng.state_hi = s1.hi;
+          c.rng.state_lo = s1.lo;
+          if (cnt & 1) {
+            c.rng.has_uint32 = 1;
+            c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);
+          } else {
+            c.rng.has_uint32 = 0;
+          }
+        }
+      }
+    }
+  } else {
+    // running-row summaries (count, sum and max of remaining) for relQueries with running rows
+    for (int e = warp - 1; e < n_est; e += kWarps - 1) {
+      const int ae = __shfl_sync(kFull, a, e);
+      const int Le = __shfl_sync(kFull, L, e);
+      const int ole = __shfl_sync(kFull, ol, e);
+      PrefixSummary ps{0, 0, 0};
+      if (Le > 0) {
+        long long rs = 0, mx = 0;
+        for (int j = lane; j < c.n_run; j += 32)
+          if (c.run_rank[j] == ae) {
+            const long long r = ole - c.run_gen[j];
+            rs += r;
+            mx = r > mx ? r : mx;
+          }
+        ps.n = Le;
+        ps.rsum = warp_sum(rs);
+        ps.rmax = (int)warp_max(mx);
+      }
+      if (lane == 0) S.est_ps[e] = ps;
+    }
+  }
+  __syncthreads();
+  phase_mark(c, 7);
+  // one warp per PEM segment
+  for (int j = warp; j < J; j += kWarps) {
+    int e = 0;
+    for (int x = 0; x < n_est; ++x)
+      if (__shfl_sync(kFull, jo, x) <= j && __shfl_sync(kFull, nj, x) > 0) e = x;
+    const int k = j - __shfl_sync(kFull, jo, e);
+    const int ne = __shfl_sync(kFull, nunp, e);
+    const int Le = __shfl_sync(kFull, L, e);
+    const int basee = __shfl_sync(kFull, base, e);
+    const int ole = __shfl_sync(kFull, ol, e);
+    const double ratio = S.est_ratio[e];
+    const long long t0l = (long long)k * pm.mns - Le, t1l = (long long)(k + 1) * pm.mns - Le;
+    const int t0 = t0l < 0 ? 0 : (int)t0l;
+    const int t1 = t1l < ne ? (int)t1l : ne;
+    const int nloc = t1 - t0;
+    int* Uw = S.small.U[warp];
+    int carry = 0;
+    for (int x0 = 0; x0 < nloc; x0 += 32) {
+      const int x = x0 + lane;
+      const int u = x < nloc ? (int)utok_approx(T.tok[basee + t0 + x], ratio) : 0;
+      const int incl = warp_incl_scan(u) + carry;
+      if (x < nloc) Uw[x] = incl;
+      carry = __shfl_sync(kFull, incl, 31);
+    }
+    __syncwarp();
+    double* tj = S.small.terms + j * kJobTerms;
+    double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
+    int nterm = 0;
+    int bb = 0;
+    while (bb < nloc) {
+      // every item is unprefilled, so every sub-batch is non-empty: one p-term each
+      const int before = bb ? Uw[bb - 1] : 0;
+      const int ub = Uw[bb];
+      const int thr = ub - before > pm.mnbt ? ub : before + (int)pm.mnbt;
+      int nb = nloc;
+      for (int b2 = bb + 1; b2 < nloc; b2 += 32) {
+        const int x = b2 + lane;
+        const unsigned msk = __ballot_sync(kFull, x < nloc && Uw[x] > thr);
+        if (msk) {
+          nb = b2 + __ffs(msk) - 1;
+          break;
+        }
+      }
+      if (lane == 0) {
+        const double t = lin(pm.ap, (double)(Uw[nb - 1] - before), pm.bp);
+        if (nterm < kJobTerms) tj[nterm] = t;
+        else spill[nterm] = t;
+      }
+      ++nterm;
+      bb = nb;
+    }
+    if (lane == 0) {
+      long long rs = (long long)nloc * ole;
+      long long mx = nloc > 0 ? ole : 0;
+      if (k == 0) {
+        rs += S.est_ps[e].rsum;
+        mx = S.est_ps[e].rmax > mx ? S.est_ps[e].rmax : mx;
+      }
+      const double t = __dadd_rn(__dmul_rn(pm.ad, (double)rs), __dmul_rn(pm.bd, (double)mx));
+      if (nterm < kJobTerms) tj[nterm] = t;
+      else spill[nterm] = t;
+      S.small.nterm[j] = nterm + 1;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  phase_mark(c, 8);
+  if (warp == 0 && lane < n_est) {  // ordered sums, relQuery by relQuery
+    double total = 0.0;
+    for (int j = jo; j < jo + nj; ++j) {
+      const int cnt = S.small.nterm[j];
+      const double* tj = S.small.terms + j * kJobTerms;
+      const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
+      for (int i = 0; i < cnt; ++i) total = __dadd_rn(total, i < kJobTerms ? tj[i] : spill[i]);
+    }
+    rq.prio[a] = total;
+  }
+  // (the caller's barrier orders these writes before the waiting order)
+  return true;
+}
+
 __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -112,6 +362,10 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
   pm.mns = cfg.max_num_seqs;
   pm.mnbt = cfg.max_num_batched_tokens;
   if (tid == 0) S.n_est = n_est;
+  if (dpu_small(P, T, S, pm)) {
+    __syncthreads();
+    goto starvation;
+  }
   for (int b0 = 0; b0 < n_est; b0 += batch) {
     const int nb = n_est - b0 < batch ? n_est - b0 : batch;
     // 1. metadata; draw, item and PEM-segment offsets in one block scan
@@ -361,6 +615,7 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
     }
     phase_mark(c, 8);
   }
+starvation:
   // starvation override (priority.py:318-339): wholly waiting = no prefilled row = q == 0
   if (isfinite(cfg.tau)) {
     for (int a = tid; a < c.n_admitted; a += kThreads) {

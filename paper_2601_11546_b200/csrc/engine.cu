@@ -776,6 +776,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_pc
   TRY(dalloc(h, &d.lde, R, nanv.data()));
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
+  TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
   d.fifo_cap = cfg->capacity_blocks + kMaxRun + 2;  // batched pushes precede evictions
   TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
   {
@@ -885,7 +886,7 @@ int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* st) {
     s.status = c->status;
     s.error_detail = c->error_detail;
     s.rng = c->rng;
-    for (int k = 0; k < 15; ++k) s.phase_cycles[k] = c->phase[k];
+    for (int k = 0; k < 23; ++k) s.phase_cycles[k] = c->phase[k];
   }
   return RS_OK;
 }

@@ -29,7 +29,11 @@ constexpr int kWin = 768;       // FIFO window of the batched prefill eviction
 constexpr int kEstBatch = 128;  // relQueries re-estimated per DPU batch
 constexpr int kDrawBuf = 4096;  // numpy next32 draws staged per DPU batch
 constexpr int kItemBuf = 2048;  // PEM items staged per segment-parallel batch
-constexpr int kPhases = 16;
+constexpr int kPhases = 24;
+constexpr int kSmallEst = 32;   // DPU fast path: at most this many re-estimated relQueries
+constexpr int kSmallMns = 256;  // ... and max_num_seqs at most this
+constexpr int kMaxJobs = 64;    // ... and at most this many PEM segments
+constexpr int kJobTerms = 32;   // fp64 terms per segment kept in shared memory (rest spill to HBM)
 
 struct FifoEnt {
   unsigned long long t0;  // touch time of the tail's first block
@@ -129,6 +133,7 @@ struct TraceDev {
   FifoEnt* fifo;
   long long fifo_cap;
   const JumpEntry* jump;  // PCG64 jump-ahead table of this trace's DPU generator
+  double* term_spill;     // [kMaxJobs * (kSmallMns + 1)] PEM terms beyond kJobTerms per segment
   rs_iter_record* log;
   long long log_cap;
   Ctl* ctl;
@@ -187,6 +192,12 @@ struct Shared {
       int REM[kItemBuf];
       int jcnt[kItemBuf + kEstBatch];
     } seg;
+    struct {
+      unsigned int draws[kSmallEst * 31];
+      double terms[kMaxJobs * kJobTerms];
+      int nterm[kMaxJobs];
+      int U[kWarps][kSmallMns];  // per-warp utok prefix of the segment it evaluates
+    } small;
     struct {
       unsigned long long t0[kWin];
       unsigned long long c0[kWin];
