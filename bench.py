@@ -46,6 +46,9 @@ PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dp
           "dpu_pem", "fp_evict_post", "prefill_post", "cand_decode", "cand_prefill", "fp_scan", "fp_stage",
           "dpu_ratio", "p16", "p17", "p18", "p19", "p20", "p21", "p22")
 WINDOW_START = 5
+#: dram__bytes_read.sum + dram__bytes_write.sum per engine_kernel launch (250 iterations) from the
+#: committed `ncu --set full` capture (profiles/r1_engine_kernel.md); None until measured
+TRAFFIC_PER_LAUNCH = 310272.0
 
 
 def parse():
@@ -173,23 +176,6 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def algorithmic_bytes(recs, c) -> float:
-    """Bytes the device scheduler must touch for these iterations (DESIGN.md
-    'Algorithmic bytes'): per iteration 20 B per admitted relQuery (priority,
-    prefilled count, row offsets: the waiting argmin), 12 B per row of each
-    re-estimated relQuery (tok, out, gen: the PEM pass), 16 B per running row
-    (decode: tok, out, gen read + gen write) and 16 B per prefilled row."""
-    sizes = np.diff(c.row_off)
-    mean_size = float(sizes.mean()) if sizes.size else 0.0
-    admitted = c.num_relqueries  # all relQueries arrive within the first iterations
-    total = 0.0
-    for r in recs:
-        total += 20.0 * admitted
-        total += 12.0 * mean_size * float(r["n_reestimated"])
-        total += 16.0 * float(r["batch_n"])
-    return total
-
-
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -219,6 +205,7 @@ def run_ours(args, ws, rank, local):
     n_read = st.n_log
     it0 = st.iterations
     ph0 = list(st.phase_cycles)
+    ab0 = st.alg_bytes
     pending0 = trace.columns().num_requests
     evs = []
     recs = []
@@ -243,6 +230,7 @@ def run_ours(args, ws, rank, local):
     st = ne.status(stream)[0]
     iters = st.iterations - it0
     ph = [a - b for a, b in zip(st.phase_cycles, ph0)]
+    alg_window = st.alg_bytes - ab0
     assert st.status == _abi.RS_RUNNING, f"trace ended inside the window (status {st.status})"
     recs = ne.read_log(0, n_read, st.n_log - n_read)
     gen, pre, comp, prio = ne.read_requests(0, trace.columns().num_requests)
@@ -253,8 +241,7 @@ def run_ours(args, ws, rank, local):
     total_iters = sum_over_ranks(float(iters), ws, dev)
     value = total_iters / (t_max / 1e3)
     c = trace.columns()
-    alg = algorithmic_bytes(recs, c)
-    per_launch_bytes = alg / args.steps
+    per_launch_bytes = alg_window / args.steps
     avg_launch_s = (t_ms / args.steps) / 1e3
     peak, peak_kind = peaks()
     achieved = per_launch_bytes / avg_launch_s / 1e9
@@ -310,8 +297,11 @@ def run_ours(args, ws, rank, local):
             "e2e": e2e,
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                         "note": "latency-bound serial iteration chain; bytes = DESIGN.md algorithmic bytes"},
+                         "frac": achieved / peak, "traffic": TRAFFIC_PER_LAUNCH, "peak_source": peak_kind,
+                         "alg_bytes_per_iter": alg_window / max(1, iters),
+                         "note": "latency-bound: one dependent iteration chain per trace; bytes = the "
+                                 "device-counted algorithmic bytes (DESIGN.md); traffic = ncu dram bytes per "
+                                 "launch of the committed profile (profiles/)"},
             "clocks": clk.summary(),
             "phase_cycles_per_iter": dict(zip(PHASES, [round(x / max(1, iters), 1) for x in ph])),
             "iteration_mix": {"prefill": int((recs["action"] == 0).sum()), "decode": int((recs["action"] == 1).sum()),

@@ -136,6 +136,9 @@ typedef struct {
      [1] priority update (DPU) remainder, [2] waiting order, [3] candidates +
      decision (ABA), [4] execution; finer marks [5..14] (see bench.py PHASES) */
   int64_t phase_cycles[23];
+  /* bytes of request / FIFO / log state the iterations had to read or write in
+     HBM (the relQuery table and running list live in shared memory) */
+  int64_t alg_bytes;
 } rs_trace_status;
 
 typedef struct rs_engine rs_engine;

@@ -88,7 +88,7 @@ class TraceStatus(C.Structure):
         ("iterations", C.c_int64), ("clock", C.c_double), ("cache_hit_tokens", C.c_int64),
         ("cache_miss_tokens", C.c_int64), ("kv_reserved", C.c_int64), ("n_log", C.c_int64),
         ("live_relqueries", C.c_int64), ("admitted", C.c_int64), ("status", C.c_int32),
-        ("error_detail", C.c_int32), ("rng", Pcg64State), ("phase_cycles", C.c_int64 * 23),
+        ("error_detail", C.c_int32), ("rng", Pcg64State), ("phase_cycles", C.c_int64 * 23), ("alg_bytes", C.c_int64),
     ]
 
 

@@ -233,6 +233,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   __syncthreads();
   phase_mark(c, 14);
   if (tid == 0) {
+    c.alg_bytes += 16LL * Wn;  // staged FIFO head
     cc_remove(c, h);
     S.fp_par = c.cc_n == 0;
     S.fp_cut = 0x7FFFFFFF;

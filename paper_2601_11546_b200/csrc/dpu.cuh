@@ -133,7 +133,13 @@ __device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const P
   const int doff = dincl - dcnt, jo = jincl - nj;
   const int D = __shfl_sync(kFull, dincl, 31), J = __shfl_sync(kFull, jincl, 31);
   if (J > kMaxJobs) return false;
-  if (tid == 0) S.n_est = n_est;
+  {
+    const int nb_items = warp_sum(nunp), nb_samp = warp_sum(nunp > Ssz ? Ssz : nunp);
+    if (tid == 0) {
+      S.n_est = n_est;
+      c.alg_bytes += 4LL * ((long long)nb_items + nb_samp);  // PEM items' tok + sampled tok
+    }
+  }
   phase_mark(c, 5);
   if (warp == 0) {
     // numpy next32 stream positions [0, D) -> bounded draws
@@ -405,6 +411,7 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
     __syncthreads();
     const int NI = S.est_io[nb];
     const bool seg = T.seg_ok && NI <= kItemBuf;
+    if (tid == 0) c.alg_bytes += 4LL * NI + 4LL * Ssz * (S.est_doff[nb] / dper);  // items' + sampled tok
     // issue the PEM items' tok loads now; they land while the RNG runs
     constexpr int kPer = kItemBuf / kThreads;
     int tokr[kPer];

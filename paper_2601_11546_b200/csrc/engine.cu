@@ -177,6 +177,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     if (tid == 0) {
       const int taken = S.first_bad < J ? S.first_bad : J;
+      const int loaded = ((S.first_bad < J ? S.first_bad : J - 1) / kThreads + 1) * kThreads;
+      c.alg_bytes += 8LL * (J < loaded ? J : loaded);  // candidate tok + out
       S.taken = taken;
       S.cand_mh = mh;
       S.utok_sum = taken > 0 ? S.cand_u[taken - 1] : 0;
@@ -260,6 +262,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     S.action = action;
     if (cfg.log_decisions && T.log_cap > 0) {
+      c.alg_bytes += sizeof(rs_iter_record);
       rs_iter_record& r = T.log[c.n_log % T.log_cap];
       r.iteration = c.iteration;
       r.clock = c.clock;
@@ -307,6 +310,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         }
       }
       if (ok) {
+        c.alg_bytes += 16LL * n;  // FIFO pushes (window reads are counted in prefill_fast)
         const double start = c.clock;
         const double dur = __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p);
         c.n_run = n_run0 + n;
@@ -415,6 +419,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     __syncthreads();
     if (tid == 0) {
+      c.alg_bytes += 8LL * (n - cbase);  // generated + completion iteration of finished rows
       c.n_run = cbase;
       c.kv -= kv_total;
       c.clock = clk;
@@ -887,6 +892,7 @@ int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* st) {
     s.error_detail = c->error_detail;
     s.rng = c->rng;
     for (int k = 0; k < 23; ++k) s.phase_cycles[k] = c->phase[k];
+    s.alg_bytes = c->alg_bytes;
   }
   return RS_OK;
 }

@@ -56,6 +56,7 @@ struct alignas(16) Ctl {
   unsigned long long tclock;  // prefix-cache touch clock (prefix_cache.py:65-68)
   long long count;            // resident blocks
   long long n_log;
+  long long alg_bytes;  // HBM/L2 bytes the algorithm must move
   long long fifo_head, fifo_tail;
   int n_admitted, live;
   int n_run, n_act;
