@@ -68,7 +68,7 @@ __device__ int cache_evict(Ctl& c, const TraceDev& T, const RqView& rq, long lon
     unsigned long long kf = ~0ULL, kc = ~0ULL;
     FifoEnt fe;
     if (have_f) {
-      fe = T.fifo[c.fifo_head % T.fifo_cap];
+      fe = T.fifo[c.fifo_head & (T.fifo_cap - 1)];
       kf = fe.t0 + (unsigned long long)(fe.tres - 1);
     }
     if (c.cc_n > 0) kc = c.cc[0].key;
@@ -88,7 +88,7 @@ __device__ int cache_evict(Ctl& c, const TraceDev& T, const RqView& rq, long lon
         if (nt == 0 && mm > 0 && !cc_insert(c, rq.c0[a] + (unsigned long long)(mm - 1), a, mm))
           return RS_EUNSUPPORTED;
       } else {
-        T.fifo[c.fifo_head % T.fifo_cap].tres = fe.tres;
+        T.fifo[c.fifo_head & (T.fifo_cap - 1)].tres = fe.tres;
       }
     } else {
       if (c.cc[0].rank == cur_rank) return RS_ECACHE_PINNED;
@@ -126,7 +126,7 @@ __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const RqView& 
     e.t0 = t0;
     e.rank = a;
     e.tres = T_len;
-    T.fifo[c.fifo_tail % T.fifo_cap] = e;
+    T.fifo[c.fifo_tail & (T.fifo_cap - 1)] = e;
     c.fifo_tail++;
     rq.ntails[a] += 1;
   } else if (Pc > 0 && rq.ntails[a] == 0) {
@@ -143,6 +143,51 @@ __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const RqView& 
     return -1;
   }
   return tok - hit;
+}
+
+// Sequential drain of E blocks in LRU order from the staged FIFO head and the
+// chain candidates (thread 0; the cold path of prefill_fast when chain
+// candidates are pending or the parallel drain's preconditions fail).
+__device__ void drain_sequential(Shared& S, const TraceDev& T, long long E, int Wn, long long head0) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  long long need = E;
+  int j = 0;
+  bool ok = true;
+  while (need > 0) {
+    const unsigned long long kf = j < Wn ? S.win.t0[j] + (unsigned long long)(S.win.tres[j] - 1) : ~0ULL;
+    const unsigned long long kc = c.cc_n > 0 ? c.cc[0].key : ~0ULL;
+    if (kf == ~0ULL && kc == ~0ULL) {
+      ok = false;
+      break;
+    }
+    if (kf < kc) {
+      const long long k = need < S.win.tres[j] ? need : S.win.tres[j];
+      S.win.tres[j] -= (int)k;
+      need -= k;
+      c.count -= k;
+      if (S.win.tres[j] == 0) {
+        const int mm = S.win.mm[j];
+        if (S.win.last[j] && mm > 0 &&
+            !cc_insert(c, S.win.c0[j] + (unsigned long long)(mm - 1), S.win.rank[j], mm)) {
+          ok = false;
+          break;
+        }
+        ++j;
+      }
+    } else {
+      const long long k = need < c.cc[0].m ? need : c.cc[0].m;
+      need -= k;
+      cc_evict_front(c, rq, k);
+    }
+  }
+  if (!ok) {
+    c.status = RS_ECACHE_PINNED;
+    c.error_detail = 4;
+  }
+  if (j < Wn) T.fifo[(head0 + j) & (T.fifo_cap - 1)].tres = S.win.tres[j];
+  S.fp_popped = j;
+  c.fifo_head = head0 + j;
 }
 
 // Batched prefill advance (all threads).  Every row of a prefill batch
@@ -210,13 +255,13 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
       e.t0 = c0i + (unsigned long long)Pc;
       e.rank = h;
       e.tres = (int)Tv[s];
-      T.fifo[(tail0 + i) % T.fifo_cap] = e;
+      T.fifo[(tail0 + i) & (T.fifo_cap - 1)] = e;
       if (i == n - 1) S.fp_c0_last = c0i;
     }
   }
   // stage the FIFO head (the oldest tails) and their relQueries' chain state
   for (int j = tid; j < Wn; j += kThreads) {
-    const FifoEnt e = T.fifo[(head0 + j) % T.fifo_cap];
+    const FifoEnt e = T.fifo[(head0 + j) & (T.fifo_cap - 1)];
     S.win.t0[j] = e.t0;
     S.win.rank[j] = e.rank;
     S.win.tres[j] = e.tres;
@@ -287,7 +332,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
           const int tr = S.win.tres[cut];
           int head_adv = cut;
           if (rem_cut < tr) {
-            T.fifo[(head0 + cut) % T.fifo_cap].tres = tr - (int)rem_cut;
+            T.fifo[(head0 + cut) & (T.fifo_cap - 1)].tres = tr - (int)rem_cut;
           } else {
             head_adv = cut + 1;
             atomicSub(&rq.ntails[a], 1);
@@ -312,45 +357,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   }
   __syncthreads();
   if (tid == 0) {
-    if (!par) {  // sequential drain in LRU order
-      long long need = E;
-      int j = 0;
-      bool ok = true;
-      while (need > 0) {
-        const unsigned long long kf = j < Wn ? S.win.t0[j] + (unsigned long long)(S.win.tres[j] - 1) : ~0ULL;
-        const unsigned long long kc = c.cc_n > 0 ? c.cc[0].key : ~0ULL;
-        if (kf == ~0ULL && kc == ~0ULL) {
-          ok = false;
-          break;
-        }
-        if (kf < kc) {
-          const long long k = need < S.win.tres[j] ? need : S.win.tres[j];
-          S.win.tres[j] -= (int)k;
-          need -= k;
-          c.count -= k;
-          if (S.win.tres[j] == 0) {
-            const int mm = S.win.mm[j];
-            if (S.win.last[j] && mm > 0 &&
-                !cc_insert(c, S.win.c0[j] + (unsigned long long)(mm - 1), S.win.rank[j], mm)) {
-              ok = false;
-              break;
-            }
-            ++j;
-          }
-        } else {
-          const long long k = need < c.cc[0].m ? need : c.cc[0].m;
-          need -= k;
-          cc_evict_front(c, rq, k);
-        }
-      }
-      if (!ok) {
-        c.status = RS_ECACHE_PINNED;
-        c.error_detail = 4;
-      }
-      if (j < Wn) T.fifo[(head0 + j) % T.fifo_cap].tres = S.win.tres[j];
-      S.fp_popped = j;
-      c.fifo_head = head0 + j;
-    }
+    if (!par) drain_sequential(S, T, E, Wn, head0);  // cold path, out of line
     const long long hitb = (long long)m0 + (long long)(n - 1) * Pc;
     c.hit += B * hitb;
     c.miss += cTok - B * hitb;

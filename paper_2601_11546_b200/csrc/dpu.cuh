@@ -92,6 +92,19 @@ __device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq
 }
 
 
+// Cold path: sequential numpy replay for relQueries [0, n_est) of this
+// iteration's estimated list (after a Lemire rejection).
+__device__ void ratios_sequential(const Params& P, const TraceDev& T, Shared& S, int e0, int n_est, int n_act) {
+  Ctl& c = S.c;
+  Pcg64 g = Pcg64::from(c.rng);
+  for (int e = 0; e < n_est; ++e) {
+    const int ge = e0 + e;
+    const int ae = ge < n_act ? c.act[ge] : S.new_lo + (ge - n_act);
+    S.est_ratio[e] = sample_ratio_seq(g, T, S.rq, P, ae);
+  }
+  c.rng = g.to();
+}
+
 // Fast path for the common steady state (few re-estimated relQueries, PEM
 // segments closed by count only, mns <= 256, sample size <= 16): two block
 // barriers in total.
@@ -104,20 +117,23 @@ __device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq
 //     sub-batch chain with ballots, and emits its terms;
 //   * lane e of warp 0 adds relQuery e's terms in the reference's order.
 // Returns false (nothing changed) when the preconditions do not hold.
-__device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const PemModel& pm) {
+// Processes the estimated relQueries [e0, e0 + n) of this iteration's list
+// (act then arrivals) for the largest n <= min(32, e1 - e0) whose PEM
+// segments fit kMaxJobs; returns n (0 if even one does not fit).
+__device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const PemModel& pm, int e0, int e1) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const rs_config& cfg = P.cfg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_act = c.n_act;
-  const int n_est = n_act + (S.new_hi - S.new_lo);
+  int n_est = e1 - e0 < kSmallEst ? e1 - e0 : kSmallEst;
   const int Ssz = (int)cfg.sample_size;
-  if (n_est > kSmallEst || !T.seg_ok || pm.mns > kSmallMns || Ssz > 16) return false;
   const int dper = 2 * Ssz - 1;
-  // per-warp metadata: lane e holds relQuery e
+  // per-warp metadata: lane e holds relQuery e0 + e
   int a = 0, base = 0, nunp = 0, ol = 0, mcb = 0, L = 0, dcnt = 0, nj = 0;
   if (lane < n_est) {
-    a = lane < n_act ? c.act[lane] : S.new_lo + (lane - n_act);
+    const int ge = e0 + lane;
+    a = ge < n_act ? c.act[ge] : S.new_lo + (ge - n_act);
     const int off = rq.off[a];
     const int q = rq.q[a];
     base = off + q;
@@ -129,16 +145,22 @@ __device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const P
     const long long tot = (long long)nunp + L;
     nj = tot > 0 ? (int)((tot + pm.mns - 1) / pm.mns) : 0;
   }
-  const int dincl = warp_incl_scan(dcnt), jincl = warp_incl_scan(nj);
+  int jincl = warp_incl_scan(nj);
+  {  // keep the prefix of relQueries whose segments fit the job buffers
+    const int fit = __popc(__ballot_sync(kFull, lane < n_est && jincl <= kMaxJobs));
+    if (fit < n_est) {
+      n_est = fit;
+      if (lane >= n_est) dcnt = nj = nunp = 0;
+      jincl = warp_incl_scan(nj);
+    }
+  }
+  if (n_est == 0) return 0;
+  const int dincl = warp_incl_scan(dcnt);
   const int doff = dincl - dcnt, jo = jincl - nj;
   const int D = __shfl_sync(kFull, dincl, 31), J = __shfl_sync(kFull, jincl, 31);
-  if (J > kMaxJobs) return false;
   {
     const int nb_items = warp_sum(nunp), nb_samp = warp_sum(nunp > Ssz ? Ssz : nunp);
-    if (tid == 0) {
-      S.n_est = n_est;
-      c.alg_bytes += 4LL * ((long long)nb_items + nb_samp);  // PEM items' tok + sampled tok
-    }
+    if (tid == 0) c.alg_bytes += 4LL * ((long long)nb_items + nb_samp);  // PEM items' tok + sampled tok
   }
   phase_mark(c, 5);
   if (warp == 0) {
@@ -151,39 +173,69 @@ __device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const P
       S.est_nunp[lane] = nunp;
     }
     __syncwarp();
-    for (int p = lane; p < D; p += 32) {
-      uint32_t v;
-      if (h0 && p == 0) {
-        v = c.rng.uinteger;
-      } else {
-        const long long pp = p - (long long)h0;
-        const uint64_t out = pcg_output(pcg_jump(s0, (unsigned long long)(pp >> 1) + 1, S.jt));
-        v = (pp & 1) ? (uint32_t)(out >> 32) : (uint32_t)out;
+    // lane l owns 64-bit output l of each 32-output round: state_{32r+l+1} =
+    // A^(l+1) state_{32r} + C_(l+1) (one 128-bit multiply-add from the
+    // consecutive-step table), whose low / high halves are next32 values
+    // 2l and 2l+1 after the buffered one
+    const int cnt32 = D - (int)h0 > 0 ? D - (int)h0 : 0;  // fresh next32 values
+    const int n64 = (cnt32 + 1) >> 1;
+    U128 sb = s0;
+    U128 s_end = s0;
+    uint64_t out_end = 0;
+    __syncwarp();
+    phase_mark(c, 16);
+    for (int r0 = 0; r0 < n64; r0 += 32) {
+      const U128 st = add128(mul128(S.jstep[lane].a, sb), S.jstep[lane].c);
+      const uint64_t out = pcg_output(st);
+      __syncwarp();
+      phase_mark(c, 17);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int p = (int)h0 + 2 * (r0 + lane) + half;
+        if (p < D) {
+          const uint32_t v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
+          int e = 0;  // relQuery owning position p: the last one with a draw offset <= p
+          for (int x = 0; x < n_est; ++x)
+            if (S.est_doff[x] <= p) e = x;
+          const int d = p - S.est_doff[e];
+          const uint32_t ne = (uint32_t)S.est_nunp[e];
+          const uint32_t bound = d < Ssz ? ne - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+          const uint32_t excl = bound + 1u;
+          const uint64_t mm = (uint64_t)v * excl;
+          const uint32_t left = (uint32_t)mm;
+          if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;  // Lemire rejection
+          S.small.draws[p] = (uint32_t)(mm >> 32);
+        }
       }
-      int e = 0;  // relQuery owning position p: the last one with a draw offset <= p
+      __syncwarp();
+      phase_mark(c, 18);
+      const int last = n64 - 1 - r0;  // lane holding the final state, if in this round
+      if (last < 32) {
+        s_end.hi = __shfl_sync(kFull, st.hi, last);
+        s_end.lo = __shfl_sync(kFull, st.lo, last);
+        out_end = __shfl_sync(kFull, out, last);
+      }
+      sb.hi = __shfl_sync(kFull, st.hi, 31);
+      sb.lo = __shfl_sync(kFull, st.lo, 31);
+    }
+    if (h0 && D > 0 && lane == 0) {  // position 0 is the buffered half-word
+      const uint32_t v = c.rng.uinteger;
+      int e = 0;
       for (int x = 0; x < n_est; ++x)
-        if (S.est_doff[x] <= p) e = x;
-      const int d = p - S.est_doff[e];
+        if (S.est_doff[x] <= 0) e = x;
       const uint32_t ne = (uint32_t)S.est_nunp[e];
-      const uint32_t bound = d < Ssz ? ne - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+      const uint32_t bound = ne - (uint32_t)Ssz;  // d = 0: Floyd's first bound n - k
       const uint32_t excl = bound + 1u;
       const uint64_t mm = (uint64_t)v * excl;
       const uint32_t left = (uint32_t)mm;
-      if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;  // Lemire rejection
-      S.small.draws[p] = (uint32_t)(mm >> 32);
+      if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;
+      S.small.draws[0] = (uint32_t)(mm >> 32);
     }
     rej = __any_sync(kFull, rej);
     __syncwarp();
     phase_mark(c, 6);
     if (rej) {  // replay sequentially: a rejection shifts every later draw
-      if (lane == 0) {
-        Pcg64 g = Pcg64::from(c.rng);
-        for (int e = 0; e < n_est; ++e) {
-          const int ae = e < n_act ? c.act[e] : S.new_lo + (e - n_act);
-          S.est_ratio[e] = sample_ratio_seq(g, T, rq, P, ae);
-        }
-        c.rng = g.to();
-      }
+      if (lane == 0) ratios_sequential(P, T, S, e0, n_est, n_act);
     } else {
       if (lane < n_est) {  // sample_cache_miss_ratio (prefix_cache.py:141-169)
         const long long mh = cfg.block_size * (long long)mcb;  // exact utok = tok - B*m
@@ -226,16 +278,14 @@ __device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const P
       __syncwarp();
       phase_mark(c, 15);
       if (lane == 0 && D > 0) {  // advance the generator past the D values
-        const long long cnt = (long long)D - (long long)h0;
-        if (cnt <= 0) {
+        if (cnt32 == 0) {
           c.rng.has_uint32 = 0;
         } else {
-          const U128 s1 = pcg_jump(s0, (unsigned long long)((cnt + 1) >> 1), S.jt);
-          c.rng.state_hi = s1.hi;
-          c.rng.state_lo = s1.lo;
-          if (cnt & 1) {
+          c.rng.state_hi = s_end.hi;
+          c.rng.state_lo = s_end.lo;
+          if (cnt32 & 1) {
             c.rng.has_uint32 = 1;
-            c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);
+            c.rng.uinteger = (uint32_t)(out_end >> 32);
           } else {
             c.rng.has_uint32 = 0;
           }
@@ -344,10 +394,112 @@ __device__ bool dpu_small(const Params& P, const TraceDev& T, Shared& S, const P
     rq.prio[a] = total;
   }
   // (the caller's barrier orders these writes before the waiting order)
-  return true;
+  return n_est;
 }
 
-__device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
+// First sight of this iteration's arrivals [new_lo, new_hi): none of their
+// rows is prefilled and their shared chain is not resident (no row of theirs
+// was ever inserted), so the sampled uncached-token ratio is exactly 1.0 and
+// utok_approx = tok: the estimate is a static function of the trace,
+// precomputed at engine creation (first_sight_kernel).  Only the RNG stream
+// must advance as the reference's choice() calls would consume it; draws are
+// replayed in parallel (jump-ahead) just to detect Lemire rejections, which
+// change how many values are consumed (then: sequential replay).
+__device__ void first_sight(const Params& P, const TraceDev& T, Shared& S, int lo, int hi) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const int tid = threadIdx.x;
+  const int Ssz = (int)P.cfg.sample_size;
+  for (int a = lo + tid; a < hi; a += kThreads) rq.prio[a] = T.fsprio[a];
+  const long long P0 = T.fs_doff[lo];
+  const long long D = T.fs_doff[hi] - P0;
+  if (tid == 0) S.rng_reject = 0;
+  __syncthreads();
+  const unsigned h0 = c.rng.has_uint32;
+  const U128 s0{c.rng.state_hi, c.rng.state_lo};
+  const long long ppt = (D + kThreads - 1) / kThreads;
+  long long p = (long long)tid * ppt;
+  const long long pend = p + ppt < D ? p + ppt : D;
+  if (p < pend) {
+    // owner of position p: the last arrival with fs_doff <= P0 + p
+    int l = lo, r = hi;  // invariant: fs_doff[l] - P0 <= p < fs_doff[r] - P0
+    while (r - l > 1) {
+      const int mid = (l + r) >> 1;
+      if (T.fs_doff[mid] - P0 <= p) l = mid;
+      else r = mid;
+    }
+    int e = l;
+    U128 st = s0;
+    uint64_t out = 0;
+    int half = 0;
+    bool fresh = true, rej = false;
+    for (; p < pend; ++p) {
+      uint32_t v;
+      if (h0 && p == 0) {
+        v = c.rng.uinteger;
+      } else {
+        if (fresh) {
+          const long long pp = p - (long long)h0;
+          st = pcg_jump(s0, (unsigned long long)(pp >> 1) + 1, S.jt);
+          out = pcg_output(st);
+          half = (int)(pp & 1);
+          fresh = false;
+        } else if (half == 0) {
+          half = 1;
+        } else {
+          st = add128(mul128(S.jt[0].a, st), S.jt[0].c);
+          out = pcg_output(st);
+          half = 0;
+        }
+        v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
+      }
+      while (T.fs_doff[e + 1] - P0 <= p) ++e;
+      const int d = (int)(p - (T.fs_doff[e] - P0));
+      const uint32_t n = (uint32_t)(rq.off[e + 1] - rq.off[e]);
+      const uint32_t bound = d < Ssz ? n - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+      const uint32_t excl = bound + 1u;
+      const uint32_t left = (uint32_t)((uint64_t)v * excl);
+      if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;
+    }
+    if (rej) S.rng_reject = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (S.rng_reject) {  // cold path: exact sequential consumption
+      Pcg64 g = Pcg64::from(c.rng);
+      for (int a = lo; a < hi; ++a) {
+        const uint32_t n = (uint32_t)(rq.off[a + 1] - rq.off[a]);
+        if (n > (uint32_t)Ssz) {
+          uint32_t idx[kMaxSample];
+          choice_floyd(g, n, (uint32_t)Ssz, idx);
+        }
+      }
+      c.rng = g.to();
+    } else if (D > 0) {
+      const long long cnt = D - (long long)h0;
+      if (cnt <= 0) {
+        c.rng.has_uint32 = 0;
+      } else {
+        const U128 s1 = pcg_jump(s0, (unsigned long long)((cnt + 1) >> 1), S.jt);
+        c.rng.state_hi = s1.hi;
+        c.rng.state_lo = s1.lo;
+        if (cnt & 1) {
+          c.rng.has_uint32 = 1;
+          c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);
+        } else {
+          c.rng.has_uint32 = 0;
+        }
+      }
+    }
+    c.alg_bytes += 12LL * (hi - lo);  // precomputed priority + draw offset per arrival
+  }
+  __syncthreads();
+}
+
+// General DPU path (first-sight batches of arrivals, many partially
+// prefilled relQueries, PEM segments that the token cap can close, or large
+// mns / sample sizes): batches of up to kEstBatch relQueries with block scans.
+__device__ void dpu_batched(const Params& P, const TraceDev& T, Shared& S, const PemModel& pm) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const rs_config& cfg = P.cfg;
@@ -359,19 +511,8 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
   const int dper = 2 * Ssz - 1;  // next32 draws of one choice(n, k=S) call without rejection
   const int batch = kDrawBuf / dper < kEstBatch ? (kDrawBuf / dper > 0 ? kDrawBuf / dper : 1) : kEstBatch;
   const long long B = cfg.block_size;
-  PemModel pm;
-  pm.ap = P.pol.alpha_p;
-  pm.bp = P.pol.beta_p;
-  pm.ad = P.pol.alpha_d;
-  pm.bd = P.pol.beta_d;
-  pm.cap = cfg.cap;
-  pm.mns = cfg.max_num_seqs;
-  pm.mnbt = cfg.max_num_batched_tokens;
   if (tid == 0) S.n_est = n_est;
-  if (dpu_small(P, T, S, pm)) {
-    __syncthreads();
-    goto starvation;
-  }
+
   for (int b0 = 0; b0 < n_est; b0 += batch) {
     const int nb = n_est - b0 < batch ? n_est - b0 : batch;
     // 1. metadata; draw, item and PEM-segment offsets in one block scan
@@ -622,7 +763,34 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
     }
     phase_mark(c, 8);
   }
-starvation:
+}
+
+template <bool kFast>
+__device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const rs_config& cfg = P.cfg;
+  const int tid = threadIdx.x;
+  PemModel pm;
+  pm.ap = P.pol.alpha_p;
+  pm.bp = P.pol.beta_p;
+  pm.ad = P.pol.alpha_d;
+  pm.bd = P.pol.beta_d;
+  pm.cap = cfg.cap;
+  pm.mns = cfg.max_num_seqs;
+  pm.mnbt = cfg.max_num_batched_tokens;
+  if constexpr (kFast) {
+    // partially prefilled relQueries (in rank order), then the arrivals
+    const int n_act = c.n_act;
+    for (int e0 = 0; e0 < n_act;) {
+      e0 += dpu_small(P, T, S, pm, e0, n_act);
+      __syncthreads();
+    }
+    if (S.new_hi > S.new_lo) first_sight(P, T, S, S.new_lo, S.new_hi);
+    if (tid == 0) S.n_est = n_act + (S.new_hi - S.new_lo);
+  } else {
+    dpu_batched(P, T, S, pm);
+  }
   // starvation override (priority.py:318-339): wholly waiting = no prefilled row = q == 0
   if (isfinite(cfg.tau)) {
     for (int a = tid; a < c.n_admitted; a += kThreads) {

@@ -42,6 +42,7 @@ namespace rsd {
 // One scheduler iteration (all threads).  Returns false when the trace stopped.
 // ---------------------------------------------------------------------------
 
+template <bool kFast>
 __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -74,7 +75,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   // ---- B: priorities.  fcfs: 0.0; sp: static_relquery_prio, both set at
   // admission (engine.py:255-267, preloaded into prio); relserve*: the DPU.
   if (P.use_dpu) {
-    dpu_update(P, T, S);
+    dpu_update<kFast>(P, T, S);
   } else if (tid == 0) {
     S.n_est = 0;
   }
@@ -263,7 +264,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     S.action = action;
     if (cfg.log_decisions && T.log_cap > 0) {
       c.alg_bytes += sizeof(rs_iter_record);
-      rs_iter_record& r = T.log[c.n_log % T.log_cap];
+      rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
       r.iteration = c.iteration;
       r.clock = c.clock;
       r.m_plus = mp;
@@ -335,7 +336,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         if (q == 0) T.fps[h] = start;  // first_prefill_start is set once (engine.py:338-339)
         T.lpe[h] = c.clock;
         if (cfg.log_decisions && T.log_cap > 0) {
-          rs_iter_record& r = T.log[c.n_log % T.log_cap];
+          rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
           r.batch_rq = h;
           r.batch_first = q;
           r.batch_n = n;
@@ -423,7 +424,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       c.n_run = cbase;
       c.kv -= kv_total;
       c.clock = clk;
-      if (cfg.log_decisions && T.log_cap > 0) T.log[c.n_log % T.log_cap].batch_n = n;
+      if (cfg.log_decisions && T.log_cap > 0) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
       if (S.rrq_dirty) {
         int w = 0;
         for (int i = 0; i < c.n_rrq; ++i)
@@ -445,7 +446,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         c.status = c.live ? RS_EABORT_IDLE : RS_OK;
         S.go = 0;
         if (cfg.log_decisions && T.log_cap > 0) {
-          T.log[c.n_log % T.log_cap].kv_reserved = c.kv;
+          T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
           c.n_log++;
         }
       } else {
@@ -459,7 +460,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   }
   if (tid == 0) {
     if (cfg.log_decisions && T.log_cap > 0) {
-      T.log[c.n_log % T.log_cap].kv_reserved = c.kv;
+      T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
       c.n_log++;
     }
     c.iteration++;
@@ -475,6 +476,7 @@ __device__ __forceinline__ void copy16(void* dst, const void* src, size_t bytes)
   for (size_t i = threadIdx.x; i < bytes / 16; i += kThreads) d[i] = s[i];
 }
 
+template <bool kFast>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ TraceDev Tsm;  // the trace's pointers, read on every access
@@ -484,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   const TraceDev& T = Tsm;
   copy16(&S.c, T.ctl, sizeof(Ctl));
   for (int i = threadIdx.x; i < kJumpBits; i += kThreads) S.jt[i] = T.jump[i];
+  for (int i = threadIdx.x; i < 32; i += kThreads) S.jstep[i] = T.jump[kJumpBits + i];
   const size_t rqb = rq_bytes(T.R);
   void* rq_base = T.rq_in_smem ? (void*)(smem_raw + ((sizeof(Shared) + 15) & ~(size_t)15)) : T.rq_global;
   if (T.rq_in_smem) copy16(rq_base, T.rq_global, rqb);
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   if (S.c.status == RS_RUNNING) {
     if (threadIdx.x == 0) S.c.phase[kPhases - 1] = clock64();
     for (long long it = 0; it < P.max_iters; ++it)
-      if (!iterate(P, T, S)) break;
+      if (!iterate<kFast>(P, T, S)) break;
   }
   __syncthreads();
   // running rows' generated counts back to HBM (finished rows were written at completion)
@@ -588,6 +591,28 @@ __global__ void choice_kernel(rs_pcg64_state* st, long long n_calls, const long 
   *st = g.to();
 }
 
+// First-sight priorities of every relQuery (one warp each, whole grid): PEM
+// of all rows with utok = tok, remaining = output_limit (see first_sight()).
+struct StaticItems {
+  const int* tok;
+  int base, ol;
+  __device__ __forceinline__ void item(int t, long long& u, int& rem, int& pre) const {
+    u = tok[base + t];
+    rem = ol;
+    pre = 0;
+  }
+};
+
+__global__ void __launch_bounds__(kThreads) first_sight_kernel(int R, const int* off, const int* ol, const int* tok,
+                                                               PemModel m, double* out) {
+  const int warps = gridDim.x * kWarps;
+  for (int a = blockIdx.x * kWarps + (threadIdx.x >> 5); a < R; a += warps) {
+    const PrefixSummary none{0, 0, 0};
+    const double v = warp_pem(StaticItems{tok, off[a], ol[a]}, off[a + 1] - off[a], none, m);
+    if ((threadIdx.x & 31) == 0) out[a] = v;
+  }
+}
+
 }  // namespace rsd
 
 // ===========================================================================
@@ -613,6 +638,7 @@ int fail(int code, const std::string& msg) {
 
 struct HostTrace {
   TraceDev dev{};
+  rs_cost_model pol{};
   std::vector<unsigned char> rq_host;  // relQuery table staging (rq_carve layout)
   std::vector<int> off;                // rank-ordered row offsets
   std::vector<int> rank_of;     // trace index -> rank
@@ -646,6 +672,7 @@ int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_by
 
 struct rs_engine {
   int device = 0;
+  bool fast = true;  // every trace qualifies for engine_kernel<true>
   Params params{};
   std::vector<HostTrace> traces;
   TraceDev* d_traces = nullptr;
@@ -679,8 +706,9 @@ static int validate_config(const rs_config* cfg) {
   return RS_OK;
 }
 
-static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_pcg64_state& rng,
-                       long long log_cap, HostTrace& h) {
+static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_cost_model& pol,
+                       const rs_pcg64_state& rng, long long log_cap, HostTrace& h) {
+  h.pol = pol;
   const long long R = v.num_relqueries, N = v.num_requests;
   if (R < 0 || N < 0 || R > 0x7FFFFFF0LL || N > 0x7FFFFFF0LL) return fail(RS_EINVAL, "trace too large");
   if (v.row_off[0] != 0 || v.row_off[R] != N) return fail(RS_EINVAL, "row_off must span [0, N]");
@@ -747,7 +775,12 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_pc
   {
     long long max_tok = 0;
     for (long long i = 0; i < N; ++i) max_tok = std::max<long long>(max_tok, tok[i]);
-    d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap;
+    d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
+    // engine_kernel<true> (no general DPU path) needs count-only PEM segments,
+    // mns and sample size within the warp fast path, and every relQuery's
+    // segments within the job buffers
+    d.fast = d.seg_ok && cfg->max_num_seqs <= kSmallMns && cfg->sample_size <= 16 &&
+             (long long)max_size + cfg->max_num_seqs <= (long long)(kMaxJobs - 1) * cfg->max_num_seqs;
   }
   int rc;
 #define TRY(x) \
@@ -782,15 +815,44 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_pc
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
   TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
-  d.fifo_cap = cfg->capacity_blocks + kMaxRun + 2;  // batched pushes precede evictions
+  {
+    // first sight (dpu.cuh first_sight): draw-count prefix on the host, the
+    // static PEM of every relQuery by one wide kernel
+    std::vector<long long> fsd(R + 1, 0);
+    const long long dper = cfg->policy >= RS_POLICY_RELSERVE ? 2 * cfg->sample_size - 1 : 0;
+    for (long long a = 0; a < R; ++a) fsd[a + 1] = fsd[a] + ((off[a + 1] - off[a]) > cfg->sample_size ? dper : 0);
+    TRY(dalloc(h, (long long**)&d.fs_doff, R + 1, fsd.data()));
+    TRY(dalloc(h, (double**)&d.fsprio, R, nullptr, 0));
+    if (R > 0 && cfg->policy >= RS_POLICY_RELSERVE) {
+      int* d_off = nullptr;
+      int* d_ol = nullptr;
+      TRY(dalloc(h, &d_off, R + 1, off.data()));
+      TRY(dalloc(h, &d_ol, R, ol.data()));
+      PemModel m{h.pol.alpha_p, h.pol.beta_p, h.pol.alpha_d, h.pol.beta_d, cfg->cap, cfg->max_num_seqs,
+                 cfg->max_num_batched_tokens};
+      const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
+      first_sight_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d.tok, m, (double*)d.fsprio);
+      cudaError_t ke = cudaGetLastError();
+      if (ke == cudaSuccess) ke = cudaDeviceSynchronize();
+      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first_sight_kernel: ") + cudaGetErrorString(ke));
+    }
+  }
+  d.fifo_cap = 1;  // >= capacity + kMaxRun + 2: batched pushes precede evictions
+  while (d.fifo_cap < cfg->capacity_blocks + kMaxRun + 2) d.fifo_cap <<= 1;
   TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
   {
-    JumpEntry tab[kJumpBits];
+    JumpEntry tab[kJumpBits + 32];
     pcg_jump_table(rng, tab);
-    TRY(dalloc(h, (JumpEntry**)&d.jump, kJumpBits, tab));
+    pcg_step_table(rng, tab + kJumpBits);
+    TRY(dalloc(h, (JumpEntry**)&d.jump, kJumpBits + 32, tab));
   }
-  d.log_cap = log_cap;
-  if (log_cap > 0) TRY(dalloc(h, &d.log, log_cap, nullptr, 0));
+  // ring capacities are powers of two so the device indexes them with a mask
+  d.log_cap = 0;
+  if (log_cap > 0) {
+    d.log_cap = 1;
+    while (d.log_cap < log_cap) d.log_cap <<= 1;
+    TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
+  }
   Ctl* ctl = (Ctl*)calloc(1, sizeof(Ctl));
   if (!ctl) return fail(RS_ENOMEM, "host alloc");
   ctl->status = RS_RUNNING;
@@ -814,7 +876,7 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
   e->device = device;
   e->traces.resize(n_traces);
   for (int t = 0; t < n_traces; ++t) {
-    rc = build_trace(traces[t], cfg, rng[t], log_capacity, e->traces[t]);
+    rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t]);
     if (rc) {
       std::string keep = g_err;
       rs_engine_destroy(e);
@@ -849,7 +911,11 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
   p.force = cfg->policy == RS_POLICY_RELSERVE_PP ? 1 : cfg->policy == RS_POLICY_RELSERVE_DP ? 2 : 0;
   p.prefill_first = cfg->policy == RS_POLICY_FCFS || cfg->policy == RS_POLICY_SP;
   e->smem = need;
-  cudaError_t ce = cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  e->fast = true;
+  for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;
+  cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  if (ce == cudaSuccess)
+    ce = cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce != cudaSuccess) {
     rs_engine_destroy(e);
     return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce));
@@ -865,7 +931,10 @@ int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
   if (e->params.cfg.log_decisions && cap > 0 && max_iters > cap) max_iters = cap;
   Params p = e->params;
   p.max_iters = max_iters;
-  engine_kernel<<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
+  if (e->fast)
+    engine_kernel<true><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
+  else
+    engine_kernel<false><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
   RS_CUDA(cudaGetLastError());
   return RS_OK;
 }

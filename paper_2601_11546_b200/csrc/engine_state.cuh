@@ -133,8 +133,11 @@ struct TraceDev {
   double* lde;
   FifoEnt* fifo;
   long long fifo_cap;
-  const JumpEntry* jump;  // PCG64 jump-ahead table of this trace's DPU generator
+  const JumpEntry* jump;  // PCG64 jump-ahead table of this trace's DPU generator: [kJumpBits] powers of two, then 32 consecutive steps
   double* term_spill;     // [kMaxJobs * (kSmallMns + 1)] PEM terms beyond kJobTerms per segment
+  const double* fsprio;   // [R] first-sight priority (static: no prefilled row, cold chain, ratio 1.0)
+  const long long* fs_doff;  // [R+1] prefix of first-sight draw counts (2S-1 per relQuery larger than S)
+  int fast;                  // engine_kernel<true> applies (see host)
   rs_iter_record* log;
   long long log_cap;
   Ctl* ctl;
@@ -161,6 +164,7 @@ struct Shared {
   RedSmem red;
   SegShared segsh;
   JumpEntry jt[kJumpBits];
+  JumpEntry jstep[32];  // (A^k, C_k) for k = 1..32 steps
   int go, action;
   int new_lo, new_hi;
   int head, W, taken, J;

@@ -162,6 +162,20 @@ inline void pcg_jump_table(const rs_pcg64_state& st, JumpEntry* tab) {
   }
 }
 
+// step[k-1] = (A^k, C_k) for k = 1..32.
+inline void pcg_step_table(const rs_pcg64_state& st, JumpEntry* step) {
+  const U128 A{PCG_MULT_HI, PCG_MULT_LO};
+  const U128 inc{st.inc_hi, st.inc_lo};
+  U128 a = A, c = inc;
+  for (int k = 1; k <= 32; ++k) {
+    step[k - 1].a = a;
+    step[k - 1].c = c;
+    // one more step: x -> A(a x + c) + inc
+    c = add128(mul128(A, c), inc);
+    a = mul128(A, a);
+  }
+}
+
 __device__ __forceinline__ U128 pcg_jump(U128 s, unsigned long long n, const JumpEntry* tab) {
   for (int i = 0; n; ++i, n >>= 1)
     if (n & 1ULL) s = add128(mul128(tab[i].a, s), tab[i].c);
