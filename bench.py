@@ -58,7 +58,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--iters-per-step", type=int, default=250)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["2", "3"], default="2")
+    ap.add_argument("--config", choices=["2", "3", "4"], default="2")
+    ap.add_argument("--traces-per-gpu", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=6000)
@@ -368,11 +369,94 @@ def run_reference(args, ws, rank):
     }
 
 
+def config4_cells():
+    """2 cost models x 16 rates (0.25..4.0) x 32 size ranges (1, s),
+    s geometric 8..1000; 100 relQueries each; seed = cell index."""
+    rates = np.geomspace(0.25, 4.0, 16)
+    sizes = np.unique(np.round(np.geomspace(8, 1000, 32)).astype(int))
+    while len(sizes) < 32:  # keep 32 distinct ranges
+        sizes = np.unique(np.append(sizes, sizes[-1] + len(sizes)))
+    cells = []
+    for model in ("opt-13b-like", "llama-70b-like"):
+        for r in rates:
+            for s in sizes[:32]:
+                cells.append((model, float(r), int(s)))
+    return cells
+
+
+def run_config4(args, ws, rank, local):
+    """Independent full runs of config-4 cells: one CTA per trace, 128 traces per GPU."""
+    import torch
+
+    from paper_2601_11546_b200 import EngineConfig, TraceConfig, _abi, _marshal, generate_trace, world_preset
+    from paper_2601_11546_b200._native import NativeEngine
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cells = config4_cells()
+    # an 8-way partition of the 1,024 cells (interleaved, so every share mixes models, rates, sizes)
+    mine = list(range(rank, len(cells), 8))[: args.traces_per_gpu]
+    cfg = EngineConfig()
+    groups = {}
+    for ci in mine:
+        model, rate, s = cells[ci]
+        t = generate_trace(TraceConfig(num_relqueries=100, size_range=(1, s), rate=rate, seed=ci))
+        groups.setdefault(model, []).append((ci, t))
+    engines = []
+    for model, items in groups.items():
+        w = world_preset(model)
+        ms = [_marshal.marshal_trace(t, cfg.block_size, "relserve", w) for _, t in items]
+        ne = NativeEngine([m.view for m in ms], _marshal.make_config(cfg, "relserve"), _marshal.make_model(w),
+                          _marshal.make_model(w), [_marshal.dpu_rng_state(ci) for ci, _ in items], local,
+                          log_capacity=0)
+        engines.append((ne, ms, torch.cuda.Stream(dev)))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    evs = []
+    with ClockSampler(local) as clk:
+        for ne, _, st in engines:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            ne.step(1 << 30, st)  # one launch runs every trace to completion
+            b.record(st)
+            evs.append((a, b))
+        torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    dev_s = max(a.elapsed_time(b) for a, b in evs) / 1e3
+    iters = 0
+    for ne, _, _ in engines:
+        for st in ne.status():
+            assert st.status == _abi.RS_OK, st.status
+            iters += st.iterations
+        ne.close()
+    t_max = max_over_ranks(dev_s, ws, dev)
+    total = sum_over_ranks(float(iters), ws, dev)
+    if rank != 0:
+        return None
+    return {
+        "metric": "sched iters/sec, config-4 sweep (aggregate over independent traces)",
+        "value": total / t_max, "unit": "iters/s", "n_gpus": ws, "steps": 1, "warmup": 0,
+        "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64+int32", "data": "synthetic (generate_trace per config-4 cell)",
+        "config": {"workload": f"config4: {args.traces_per_gpu} traces/GPU of 100 relQ, sizes (1,s) s=8..1000, "
+                               "rates 0.25..4, opt-13b/llama-70b, full runs", "traces_per_gpu": len(mine)},
+        "iterations_timed": int(total), "gpu_launches": len(engines), "clocks": clk.summary(),
+        "host_wall_s": wall,
+    }
+
+
 def main():
     args = parse()
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         out = run_reference(args, ws, rank)
+    elif args.config == "4":
+        out = run_config4(args, ws, rank, local)
     else:
         out = run_ours(args, ws, rank, local)
     if rank == 0 and out is not None:

@@ -194,6 +194,9 @@ void rs_engine_destroy(rs_engine* e);
 /* Device bytes held per trace (SoA + scratch), for reporting. */
 int64_t rs_engine_device_bytes(const rs_engine* e);
 
+/* SM clock of `device` in kHz (converts rs_trace_status.phase_cycles to seconds). */
+int rs_device_clock_khz(int32_t device);
+
 /* ---------------------------------------------------------------------------
  * Unit entry points (parity tests); same device code as the engine.
  * ------------------------------------------------------------------------- */

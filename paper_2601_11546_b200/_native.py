@@ -56,6 +56,8 @@ def lib():
     L.rs_pem_batch.restype = C.c_int
     L.rs_pem_batch.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                C.c_int64, C.c_int64, C.POINTER(_abi.CostModel), C.c_void_p, C.c_int32]
+    L.rs_device_clock_khz.restype = C.c_int
+    L.rs_device_clock_khz.argtypes = [C.c_int32]
     L.rs_choice_sequence.restype = C.c_int
     L.rs_choice_sequence.argtypes = [C.POINTER(_abi.Pcg64State), C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_int32]
@@ -67,8 +69,12 @@ def lib():
 EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_build_info", "rs_engine_create", "rs_engine_step", "rs_engine_status",
     "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_destroy",
-    "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence",
+    "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
 )
+
+
+def device_clock_khz(device: int = 0) -> int:
+    return int(lib().rs_device_clock_khz(device))
 
 
 def _check(rc: int):
@@ -133,6 +139,11 @@ class NativeEngine:
         _check(lib().rs_engine_read_requests(self.h, t, gen.ctypes.data, pre.ctypes.data,
                                              comp.ctypes.data, prio.ctypes.data))
         return gen, pre, comp, prio
+
+    def read_completion(self, t: int, N: int) -> np.ndarray:
+        comp = np.zeros(N, np.int64)
+        _check(lib().rs_engine_read_requests(self.h, t, None, None, comp.ctypes.data, None))
+        return comp
 
     def device_bytes(self) -> int:
         return int(lib().rs_engine_device_bytes(self.h))

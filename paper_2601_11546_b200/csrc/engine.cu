@@ -1016,21 +1016,22 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
   const HostTrace& h = e->traces[t];
   const int R = h.dev.R, N = h.dev.N;
   RS_CUDA(cudaSetDevice(e->device));
-  std::vector<int> gen(N), comp(N);
+  std::vector<int> gen(generated ? N : 0), comp(completion_iter ? N : 0);
   std::vector<unsigned char> tab(h.rq_host.size());
-  if (N) {
-    RS_CUDA(cudaMemcpy(gen.data(), h.dev.gen, N * 4, cudaMemcpyDeviceToHost));
-    RS_CUDA(cudaMemcpy(comp.data(), h.dev.comp, N * 4, cudaMemcpyDeviceToHost));
-  }
-  RS_CUDA(cudaMemcpy(tab.data(), h.dev.rq_global, tab.size(), cudaMemcpyDeviceToHost));
+  if (N && generated) RS_CUDA(cudaMemcpy(gen.data(), h.dev.gen, N * 4, cudaMemcpyDeviceToHost));
+  if (N && completion_iter) RS_CUDA(cudaMemcpy(comp.data(), h.dev.comp, N * 4, cudaMemcpyDeviceToHost));
+  if (prefilled || priority) RS_CUDA(cudaMemcpy(tab.data(), h.dev.rq_global, tab.size(), cudaMemcpyDeviceToHost));
   const RqView v = rq_carve(tab.data(), R);
   for (int a = 0; a < R; ++a) {
-    for (int k = h.off[a]; k < h.off[a + 1]; ++k) {
+    const int lo = h.off[a], hi = h.off[a + 1];
+    const int qa = (prefilled || priority) ? v.q[a] : 0;
+    const double pa = priority ? v.prio[a] : 0.0;
+    for (int k = lo; k < hi; ++k) {
       const long long src = h.row_src[k];
       if (generated) generated[src] = gen[k];
-      if (prefilled) prefilled[src] = (k - h.off[a]) < v.q[a];
+      if (prefilled) prefilled[src] = (k - lo) < qa;
       if (completion_iter) completion_iter[src] = comp[k];
-      if (priority) priority[src] = v.prio[a];
+      if (priority) priority[src] = pa;
     }
   }
   return RS_OK;
@@ -1043,6 +1044,12 @@ void rs_engine_destroy(rs_engine* e) {
     for (void* p : h.allocs) cudaFree(p);
   if (e->d_traces) cudaFree(e->d_traces);
   delete e;
+}
+
+int rs_device_clock_khz(int32_t device) {
+  int khz = 0;
+  if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess) return 0;
+  return khz;
 }
 
 int64_t rs_engine_device_bytes(const rs_engine* e) {

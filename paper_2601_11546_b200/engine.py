@@ -142,6 +142,13 @@ def _opt(x: float):
     return None if math.isnan(x) else float(x)
 
 
+#: rs_trace_status.phase_cycles slots of the priority update (DPU) and of the
+#: waiting order + candidates + decision (ABA), mirroring the reference's
+#: dpu_wall / aba_wall timers (engine.py:381-417); see csrc phase_mark calls
+_DPU_PHASES = (1, 5, 6, 7, 8, 15, 16, 17, 18)
+_ABA_PHASES = (2, 3, 11, 12)
+
+
 _ERRORS = {
     _abi.RS_EINVAL: ValueError,
     _abi.RS_EINFEASIBLE: InfeasibleRequestError,
@@ -248,43 +255,58 @@ class Engine:
         st = self._status
         c = self.trace.columns()
         arrival, fps, lpe, lde = ne.read_ledgers(0, c.num_relqueries)
-        gen, pre, comp, prio = ne.read_requests(0, c.num_requests)
+        comp = ne.read_completion(0, c.num_requests)
         order = np.lexsort((c.rel_id, c.arrival))
         admitted = np.zeros(c.num_relqueries, bool)
         admitted[order[: st.admitted]] = True
         ledgers = {}
+        rid, av, fv, lv, dv = (c.rel_id.tolist(), arrival.tolist(), fps.tolist(), lpe.tolist(), lde.tolist())
         for i in order[: st.admitted].tolist():
-            ledgers[int(c.rel_id[i])] = TimestampLedger(
-                float(arrival[i]), _opt(fps[i]), _opt(lpe[i]), _opt(lde[i]))
+            ledgers[rid[i]] = TimestampLedger(av[i], _opt(fv[i]), _opt(lv[i]), _opt(dv[i]))
         recs = (np.concatenate(self._records) if self._records
                 else np.zeros(0, _abi.ITER_RECORD_DTYPE))
         log = []
-        if self.config.log_decisions:
-            for r in recs:
-                proj = not math.isnan(r["delta_plus"])
+        if self.config.log_decisions and len(recs):
+            cols = {k: recs[k].tolist() for k in ("iteration", "clock", "kase", "m_plus", "m_minus",
+                                                  "delta_plus", "delta_minus", "delta_total", "action")}
+            nan = math.isnan
+            for it, clk, ks, mp, mm, dp, dm, dt, ac in zip(*cols.values()):
+                proj = not nan(dp)
                 log.append(DecisionLogEntry(
-                    int(r["iteration"]), float(r["clock"]), _abi.CASES[r["kase"]],
-                    _opt(r["m_plus"]), _opt(r["m_minus"]),
-                    float(r["delta_plus"]) if proj else None,
-                    float(r["delta_minus"]) if proj else None,
-                    float(r["delta_total"]) if proj else None,
-                    _abi.ACTIONS[r["action"]]))
-        if self.trace.materialized:
+                    it, clk, _abi.CASES[ks], None if nan(mp) else mp, None if nan(mm) else mm,
+                    dp if proj else None, dm if proj else None, dt if proj else None, _abi.ACTIONS[ac]))
+        self._requests_state = None
+        if self.trace.materialized:  # reference semantics: the run mutates the Request objects
+            gen, pre, _, prio = self.requests_state
             k = 0
             g, p, pr = gen.tolist(), pre.tolist(), prio.tolist()
             for q in self.trace.entries:
                 for r in q.requests:
                     r.generated, r.prefilled, r.priority = g[k], bool(p[k]), pr[k]
                     k += 1
-        self.requests_state = (gen, pre, comp, prio)
         return RunResult(
             policy=self.policy, rate=self.trace.rate, seed=self.seed, ledgers=ledgers,
             relquery_sizes={int(r): int(s) for r, s in zip(c.rel_id.tolist(), np.diff(c.row_off).tolist())},
             decision_log=log, iterations=int(st.iterations), sim_duration=float(st.clock),
-            dpu_wall_s=0.0, aba_wall_s=0.0, cache_hit_tokens=int(st.cache_hit_tokens),
+            dpu_wall_s=self._phase_seconds(st, _DPU_PHASES), aba_wall_s=self._phase_seconds(st, _ABA_PHASES),
+            cache_hit_tokens=int(st.cache_hit_tokens),
             cache_miss_tokens=int(st.cache_miss_tokens), completion_iteration=comp, records=recs,
             device_wall_s=wall,
         )
+
+    @property
+    def requests_state(self):
+        """(generated, prefilled, completion_iteration, priority) per request, trace order."""
+        if getattr(self, "_requests_state", None) is None:
+            self._requests_state = self._native.read_requests(0, self.trace.columns().num_requests)
+        return self._requests_state
+
+    def _phase_seconds(self, st, phases) -> float:
+        """Device time of the given phases (clock64 cycles / SM clock)."""
+        from . import _native
+
+        khz = _native.device_clock_khz(self.device)
+        return sum(int(st.phase_cycles[k]) for k in phases) / (khz * 1e3) if khz else 0.0
 
     @property
     def running(self) -> list:
