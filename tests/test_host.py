@@ -1,0 +1,97 @@
+"""Host-side logic (no GPU): trace generation and files, prefix-structure
+marshalling, static priorities, API validation and the no-fallback rule."""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2601_11546_b200 import (ArrivalTrace, EngineConfig, RelQuery, Request, TraceConfig,
+                                   generate_heavy_tail_trace, generate_trace, load_trace, save_trace,
+                                   static_relquery_prio, world_preset)
+from paper_2601_11546_b200 import _marshal
+from paper_2601_11546_b200.engine import Engine, SimulationAborted
+from golden_util import digest_columns, digest_entries
+
+
+def test_v1_round_trip_is_identical(tmp_path):
+    t = generate_trace(TraceConfig(num_relqueries=20, size_range=(1, 30), rate=2.0, seed=5))
+    p = tmp_path / "t.jsonl"
+    save_trace(t, p)
+    t2 = load_trace(p)
+    assert digest_columns(t.columns()) == digest_columns(t2.columns())
+    save_trace(t2, tmp_path / "t2.jsonl")
+    assert p.read_bytes() == (tmp_path / "t2.jsonl").read_bytes()
+
+
+def test_lazy_tokens_follow_the_count_keyed_streams():
+    t = generate_trace(TraceConfig(num_relqueries=3, size_range=(4, 4), rate=1.0, seed=2))
+    for q in t.entries:
+        toks = [r.tokens for r in q.requests]
+        assert all(len(x) == r.tok for x, r in zip(toks, q.requests))
+        pre = toks[0][: q.prefix_len]
+        assert all(x[: q.prefix_len] == pre for x in toks)  # shared prefix
+        # the first suffix tokens differ between rows (private tails)
+        assert len({tuple(x[q.prefix_len:q.prefix_len + 4]) for x in toks}) == len(toks)
+    # entries built from columns and columns rebuilt from entries agree
+    assert digest_entries(t.entries) == digest_columns(t.columns())
+
+
+def test_heavy_tail_trace_is_deterministic_and_bounded():
+    a = generate_heavy_tail_trace(num_relqueries=300, seed=4)
+    b = generate_heavy_tail_trace(num_relqueries=300, seed=4)
+    assert digest_columns(a.columns()) == digest_columns(b.columns())
+    ol = a.columns().output_limit
+    assert ol.min() >= 8 and ol.max() <= 2048 and (ol > 100).any()
+
+
+def _rq(rel_id, rows, limit=5, arrival=0.0):
+    return RelQuery(rel_id, [Request(rel_id, i, toks, limit, limit, arrival) for i, toks in enumerate(rows)],
+                    limit, arrival)
+
+
+def test_chain_blocks_from_explicit_tokens():
+    shared = list(range(100, 132))  # two whole blocks shared by every row
+    rows = [shared + [1000 * i + j for j in range(20)] for i in range(1, 4)]
+    t = ArrivalTrace([_rq(0, rows)], 1.0, 0)
+    m = _marshal.marshal_trace(t, 16, "relserve", world_preset("opt-13b-like"))
+    assert m.arrays["chain_blocks"].tolist() == [2]
+
+
+def test_non_forest_prefix_structure_is_rejected():
+    shared = list(range(64))
+    a = _rq(0, [shared + [1, 2, 3], shared + [4, 5, 6]])
+    b = _rq(1, [shared + [7, 8, 9]])  # shares blocks with relQuery 0
+    t = ArrivalTrace([a, b], 1.0, 0)
+    with pytest.raises(NotImplementedError):
+        _marshal.marshal_trace(t, 16, "relserve", world_preset("opt-13b-like"))
+
+
+def test_static_priorities_match_python_sum():
+    t = generate_trace(TraceConfig(num_relqueries=25, size_range=(1, 60), rate=3.0, seed=9))
+    m = world_preset("qwen-32b-like")
+    got = _marshal._static_priorities(t, m, None)
+    for q, g in zip(t.entries, got):
+        want = static_relquery_prio(q, lambda tok: m.alpha_p * tok, lambda ol: m.alpha_d * ol)
+        assert g == want  # bit-exact, incl. CPython 3.12's compensated sum
+
+
+def test_api_validation_before_any_device_work():
+    t = generate_trace(TraceConfig(num_relqueries=2, size_range=(1, 3), seed=1))
+    w = world_preset("opt-13b-like")
+    with pytest.raises(ValueError):
+        Engine(t, "srpt", w)
+    with pytest.raises(ValueError):
+        Engine(t, "relserve", w, EngineConfig(tau=0.0))
+    with pytest.raises(NotImplementedError):
+        Engine(t, "relserve", w, EngineConfig(noise_sigma=0.1))
+
+
+def test_no_cpu_fallback_without_a_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    t = generate_trace(TraceConfig(num_relqueries=2, size_range=(1, 3), seed=1))
+    with pytest.raises(RuntimeError):
+        Engine(t, "relserve", world_preset("opt-13b-like"))
