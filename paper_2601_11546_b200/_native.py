@@ -15,7 +15,7 @@ import numpy as np
 from . import _abi
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "lib" / "librelserve_b200.so"
+LIB_PATH = Path(os.environ["RS_LIB"]) if os.environ.get("RS_LIB") else HERE / "lib" / "librelserve_b200.so"
 
 _lib = None
 

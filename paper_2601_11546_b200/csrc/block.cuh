@@ -9,6 +9,16 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// Warp index the compiler cannot relate to threadIdx.x.  Without it, nvcc
+// jump-threads an `if (threadIdx.x == 0) {...}` straight into a following
+// `if (warp == 0) {...}` body without a reconvergence point, and warp 0 then
+// runs the whole warp-specialised section twice (lane 0, then lanes 1-31).
+__device__ __forceinline__ int opaque_warp() {
+  unsigned t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return (int)(t >> 5);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
   const int lane = threadIdx.x & 31;

@@ -124,7 +124,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const rs_config& cfg = P.cfg;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = opaque_warp();
   const int n_act = c.n_act;
   int n_est = e1 - e0 < kSmallEst ? e1 - e0 : kSmallEst;
   const int Ssz = (int)cfg.sample_size;
@@ -142,8 +142,8 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     mcb = rq.m[a];
     L = rq.nrun[a];  // running rows = the live prefilled rows (prefilled summary)
     dcnt = nunp > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
-    const long long tot = (long long)nunp + L;
-    nj = tot > 0 ? (int)((tot + pm.mns - 1) / pm.mns) : 0;
+    const int tot = nunp + L, mns = (int)pm.mns;  // 32-bit: rows per relQuery < 2^31
+    nj = tot > 0 ? (tot + mns - 1) / mns : 0;
   }
   int jincl = warp_incl_scan(nj);
   {  // keep the prefix of relQueries whose segments fit the job buffers
@@ -332,13 +332,26 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     const int t1 = t1l < ne ? (int)t1l : ne;
     const int nloc = t1 - t0;
     int* Uw = S.small.U[warp];
-    int carry = 0;
-    for (int x0 = 0; x0 < nloc; x0 += 32) {
-      const int x = x0 + lane;
-      const int u = x < nloc ? (int)utok_approx(T.tok[basee + t0 + x], ratio) : 0;
-      const int incl = warp_incl_scan(u) + carry;
-      if (x < nloc) Uw[x] = incl;
-      carry = __shfl_sync(kFull, incl, 31);
+    {  // utok prefix of the segment: lane l owns items [l*per, l*per + per), per <= 8
+      // (nloc <= mns <= kSmallMns); all loads issue at once, one warp scan
+      static_assert(kSmallMns <= 8 * 32, "items per lane");
+      const int per = (nloc + 31) >> 5;
+      const int x0 = lane * per;
+      int uv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) uv[i] = (i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
+      int ls = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uv[i] = uv[i] ? (int)utok_approx(uv[i], ratio) : 0;
+        ls += uv[i];
+      }
+      int run = warp_incl_scan(ls) - ls;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        run += uv[i];
+        if (i < per && x0 + i < nloc) Uw[x0 + i] = run;
+      }
     }
     __syncwarp();
     double* tj = S.small.terms + j * kJobTerms;
@@ -503,7 +516,7 @@ __device__ void dpu_batched(const Params& P, const TraceDev& T, Shared& S, const
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const rs_config& cfg = P.cfg;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = opaque_warp();
   const int n_act = c.n_act;
   const int n_new = S.new_hi - S.new_lo;
   const int n_est = n_act + n_new;

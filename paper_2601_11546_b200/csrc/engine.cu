@@ -61,7 +61,10 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     } else {
       int a = c.n_admitted;
       const int a0 = a;
-      while (a < T.R && rq.arrival[a] <= c.clock) ++a;
+      while (a < T.R && rq.arrival[a] <= c.clock) {
+        c.n_wait += rq.off[a + 1] > rq.off[a];  // a waiting entry iff it has rows
+        ++a;
+      }
       c.live += a - a0;
       c.n_admitted = a;
       S.new_lo = a0;
@@ -82,26 +85,102 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   phase_mark(c, 1);
 
   // ---- C: waiting head = argmin (prio, rank) over relQueries with pending
-  // rows, and W = len(waiting); one fused block reduction
+  // rows, and W = len(waiting) (engine.py:277-281).  A relQuery none of whose
+  // rows was prefilled keeps a static priority (first-sight estimate reused,
+  // priority.py:261-266, 298-302; sp/fcfs: fixed at admission), so those are
+  // visited in a precomputed (priority bits, rank) order (rq.zl): the first
+  // admitted one is their minimum.  Every warp runs the same scan (no
+  // barrier); only the re-estimated (partially prefilled) relQueries are
+  // compared by value.  Starvation overrides (finite tau) or a long run of
+  // not-yet-admitted entries fall back to one block reduction over all.
   int head_l;
+  int zptr_new = c.zptr;
   {
+    const int lane = tid & 31;
     unsigned long long key = ~0ULL;
     int idx = 0x7FFFFFFF;
-    int w = 0;
-    for (int a = tid; a < c.n_admitted; a += kThreads) {
-      if (rq.q[a] < rq.off[a + 1] - rq.off[a]) {
-        ++w;
-        const unsigned long long k = dbits(rq.prio[a]);
-        if (k < key) {  // ranks visited in increasing order: strict < keeps the smallest rank
-          key = k;
-          idx = a;
+    bool full = !P.zorder;
+    if (P.zorder) {
+      int i0 = c.zptr;
+      bool lead = true;
+      for (int round = 0;; ++round) {
+        if (i0 >= T.R) break;
+        if (round == kZScanRounds) {
+          full = true;
+          break;
+        }
+        const int i = i0 + lane;
+        bool gone = true, elig = false;
+        int a = 0;
+        if (i < T.R) {
+          a = rq.zl[i];
+          const int q = rq.q[a], sz = rq.off[a + 1] - rq.off[a];
+          // DPU policies: leaves the static order at its first prefill; sp/fcfs: when fully prefilled
+          gone = P.use_dpu ? (q > 0 || sz == 0) : q >= sz;
+          elig = !gone && a < c.n_admitted;
+        }
+        if (lead) {
+          const unsigned keep = ~__ballot_sync(kFull, gone);
+          if (keep == 0) {
+            zptr_new = i0 + 32 < T.R ? i0 + 32 : T.R;
+          } else {
+            zptr_new = i0 + __ffs(keep) - 1;
+            lead = false;
+          }
+        }
+        const unsigned em = __ballot_sync(kFull, elig);
+        if (em) {
+          idx = __shfl_sync(kFull, a, __ffs(em) - 1);
+          key = dbits(rq.prio[idx]);
+          break;
+        }
+        i0 += 32;
+      }
+      if (P.use_dpu) {  // partially prefilled relQueries with pending rows
+        for (int j = lane; j < c.n_act; j += 32) {
+          const int a = c.act[j];
+          if (rq.q[a] < rq.off[a + 1] - rq.off[a]) {
+            const unsigned long long k = dbits(rq.prio[a]);
+            if (k < key || (k == key && a < idx)) {
+              key = k;
+              idx = a;
+            }
+          }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+          const unsigned long long ok = __shfl_xor_sync(kFull, key, d);
+          const int oi = __shfl_xor_sync(kFull, idx, d);
+          if (ok < key || (ok == key && oi < idx)) {
+            key = ok;
+            idx = oi;
+          }
         }
       }
     }
-    block_count_argmin(w, key, idx, S.red);  // result is block-uniform in registers
-    head_l = w > 0 ? idx : -1;
+    if (full) {
+      int w = 0;
+      key = ~0ULL;
+      idx = 0x7FFFFFFF;
+      for (int a = tid; a < c.n_admitted; a += kThreads) {
+        if (rq.q[a] < rq.off[a + 1] - rq.off[a]) {
+          ++w;
+          const unsigned long long k = dbits(rq.prio[a]);
+          if (k < key) {  // ranks visited in increasing order: strict < keeps the smallest rank
+            key = k;
+            idx = a;
+          }
+        }
+      }
+      block_count_argmin(w, key, idx, S.red);  // result is block-uniform in registers
+    }
+    head_l = c.n_wait > 0 && idx != 0x7FFFFFFF ? idx : -1;
     if (tid == 0) {
-      S.W = w;
+      if (c.n_wait > 0 && head_l < 0) {  // internal inconsistency: never expected
+        c.status = RS_EUNSUPPORTED;
+        c.error_detail = 9;
+      }
+      S.W = c.n_wait;
       S.head = head_l;  // read by other threads only after later barriers
     }
   }
@@ -262,6 +341,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       }
     }
     S.action = action;
+    c.zptr = zptr_new;
     if (cfg.log_decisions && T.log_cap > 0) {
       c.alg_bytes += sizeof(rs_iter_record);
       rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
@@ -316,6 +396,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         const double dur = __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p);
         c.n_run = n_run0 + n;
         rq.q[h] = q + n;
+        if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
         if (rq.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
         rq.nrun[h] += n;
         if (q == 0 && P.use_dpu) {  // becomes partially prefilled: join the re-estimate list
@@ -785,27 +866,6 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   int rc;
 #define TRY(x) \
   if ((rc = (x))) return rc
-  // relQuery table (rq_carve layout), uploaded as one block
-  {
-    // rank of each rel_id among all rel_ids: the Delta projection's sort key
-    std::vector<int> byid(R);
-    std::iota(byid.begin(), byid.end(), 0);
-    std::stable_sort(byid.begin(), byid.end(), [&](int x, int y) { return relid[x] < relid[y]; });
-    h.rq_host.assign(rq_bytes((int)R) + 16, 0);
-    RqView hv = rq_carve(h.rq_host.data(), (int)R);
-    for (long long a = 0; a < R; ++a) {
-      hv.prio[a] = cfg->policy == RS_POLICY_SP ? sprio[a] : 0.0;  // sp/fcfs priority at admission
-      hv.arrival[a] = arrival[a];
-      hv.off[a] = off[a];
-      hv.ol[a] = ol[a];
-      hv.chain[a] = chain[a];
-      hv.scr_last[a] = -1;
-    }
-    hv.off[R] = off[R];
-    for (long long i = 0; i < R; ++i) hv.relrank[byid[i]] = (int)i;
-    TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
-    h.off.assign(off.begin(), off.end());
-  }
   TRY(dalloc(h, (int**)&d.tok, N, tok.data()));
   TRY(dalloc(h, (int**)&d.out, N, out.data()));
   std::vector<double> nanv(R, NAN);
@@ -836,6 +896,47 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       if (ke == cudaSuccess) ke = cudaDeviceSynchronize();
       if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first_sight_kernel: ") + cudaGetErrorString(ke));
     }
+  }
+  // relQuery table (rq_carve layout), uploaded as one block
+  {
+    // rank of each rel_id among all rel_ids: the Delta projection's sort key
+    std::vector<int> byid(R);
+    std::iota(byid.begin(), byid.end(), 0);
+    std::stable_sort(byid.begin(), byid.end(), [&](int x, int y) { return relid[x] < relid[y]; });
+    h.rq_host.assign(rq_bytes((int)R) + 16, 0);
+    RqView hv = rq_carve(h.rq_host.data(), (int)R);
+    for (long long a = 0; a < R; ++a) {
+      hv.prio[a] = cfg->policy == RS_POLICY_SP ? sprio[a] : 0.0;  // sp/fcfs priority at admission
+      hv.arrival[a] = arrival[a];
+      hv.off[a] = off[a];
+      hv.ol[a] = ol[a];
+      hv.chain[a] = chain[a];
+      hv.scr_last[a] = -1;
+    }
+    hv.off[R] = off[R];
+    for (long long i = 0; i < R; ++i) hv.relrank[byid[i]] = (int)i;
+    // static waiting order: a never-prefilled relQuery's priority is its
+    // first-sight estimate (DPU policies), its static priority (sp) or 0 (fcfs)
+    {
+      std::vector<double> zp(R, 0.0);
+      if (cfg->policy == RS_POLICY_SP) {
+        zp = sprio;
+      } else if (dpu && R > 0) {
+        cudaError_t ce = cudaMemcpy(zp.data(), d.fsprio, R * sizeof(double), cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("first-sight readback: ") + cudaGetErrorString(ce));
+      }
+      std::vector<int> z(R);
+      std::iota(z.begin(), z.end(), 0);
+      auto bits = [&](int a) {
+        unsigned long long b;
+        memcpy(&b, &zp[a], 8);
+        return b;
+      };
+      std::stable_sort(z.begin(), z.end(), [&](int x, int y) { return bits(x) < bits(y); });
+      for (long long i = 0; i < R; ++i) hv.zl[i] = z[i];
+    }
+    TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
+    h.off.assign(off.begin(), off.end());
   }
   d.fifo_cap = 1;  // >= capacity + kMaxRun + 2: batched pushes precede evictions
   while (d.fifo_cap < cfg->capacity_blocks + kMaxRun + 2) d.fifo_cap <<= 1;
@@ -910,6 +1011,7 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
   p.use_dpu = cfg->policy >= RS_POLICY_RELSERVE;
   p.force = cfg->policy == RS_POLICY_RELSERVE_PP ? 1 : cfg->policy == RS_POLICY_RELSERVE_DP ? 2 : 0;
   p.prefill_first = cfg->policy == RS_POLICY_FCFS || cfg->policy == RS_POLICY_SP;
+  p.zorder = !p.use_dpu || std::isinf(cfg->tau);
   e->smem = need;
   e->fast = true;
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;

@@ -33,7 +33,8 @@ constexpr int kPhases = 24;
 constexpr int kSmallEst = 32;   // DPU fast path: at most this many re-estimated relQueries
 constexpr int kSmallMns = 256;  // ... and max_num_seqs at most this
 constexpr int kMaxJobs = 64;    // ... and at most this many PEM segments
-constexpr int kJobTerms = 32;   // fp64 terms per segment kept in shared memory (rest spill to HBM)
+constexpr int kJobTerms = 32;
+constexpr int kZScanRounds = 8;  // static-order scan: 32-entry rounds before the full reduction   // fp64 terms per segment kept in shared memory (rest spill to HBM)
 
 struct FifoEnt {
   unsigned long long t0;  // touch time of the tail's first block
@@ -60,6 +61,7 @@ struct alignas(16) Ctl {
   long long fifo_head, fifo_tail;
   int n_admitted, live;
   int n_run, n_act;
+  int zptr, n_wait;  // static-order scan start (zl entries before it are prefilled); len(waiting)
   int status, error_detail;
   int cc_n, n_rrq;
   rs_pcg64_state rng;
@@ -92,12 +94,13 @@ struct RqView {
   int* relrank;  // rank of the relQuery's rel_id among all rel_ids (tie order)
   int* scr_cnt;
   int* scr_last;
+  int* zl;  // ranks sorted by (static priority bits, rank): the order of never-prefilled relQueries
 };
 
 // bytes of the relQuery table for R relQueries (16-byte aligned sections)
 __host__ __device__ inline size_t rq_bytes(int R) {
   auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
-  return 3 * al(8 * (size_t)R) + al(4 * ((size_t)R + 1)) + 10 * al(4 * (size_t)R);
+  return 3 * al(8 * (size_t)R) + al(4 * ((size_t)R + 1)) + 11 * al(4 * (size_t)R);
 }
 
 __host__ __device__ inline RqView rq_carve(void* base, int R) {
@@ -112,8 +115,9 @@ __host__ __device__ inline RqView rq_carve(void* base, int R) {
   p += al(8 * (size_t)R);
   v.off = (int*)p;
   p += al(4 * ((size_t)R + 1));
-  int** ints[10] = {&v.q, &v.m, &v.ntails, &v.nrun, &v.ndone, &v.ol, &v.chain, &v.relrank, &v.scr_cnt, &v.scr_last};
-  for (int i = 0; i < 10; ++i) {
+  int** ints[11] = {&v.q, &v.m, &v.ntails, &v.nrun, &v.ndone, &v.ol, &v.chain, &v.relrank, &v.scr_cnt, &v.scr_last,
+                    &v.zl};
+  for (int i = 0; i < 11; ++i) {
     *ints[i] = (int*)p;
     p += al(4 * (size_t)R);
   }
@@ -151,7 +155,7 @@ struct Params {
   int use_dpu;
   int force;  // 0 none, 1 prefill (relserve-pp), 2 decode (relserve-dp)
   int prefill_first;
-  int pad;
+  int zorder;  // waiting head from the static order (no starvation override possible)
   long long max_iters;
 };
 
@@ -221,17 +225,20 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7FF8000000000000LL); }
 
-// thread 0 accumulates the cycles since the previous mark into phase k
-// (-DRS_PHASE_TIMERS=0 compiles them out; measured cost at config 2 is below noise)
+// thread 0 accumulates the cycles since the previous mark into phase k.
+// RS_PHASE_TIMERS: 0 off, 1 the five coarse phases (0-4: admission, DPU,
+// waiting order, candidates + decision, execution), 2 also the fine marks.
 #ifndef RS_PHASE_TIMERS
 #define RS_PHASE_TIMERS 1
 #endif
 __device__ __forceinline__ void phase_mark(Ctl& c, int k) {
 #if RS_PHASE_TIMERS
-  if (threadIdx.x == 0) {
-    const long long now = clock64();
-    c.phase[k] += now - c.phase[kPhases - 1];
-    c.phase[kPhases - 1] = now;
+  if (RS_PHASE_TIMERS >= 2 || k < 5) {
+    if (threadIdx.x == 0) {
+      const long long now = clock64();
+      c.phase[k] += now - c.phase[kPhases - 1];
+      c.phase[kPhases - 1] = now;
+    }
   }
 #else
   (void)c;
