@@ -314,32 +314,43 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       if (lane == 0) S.est_ps[e] = ps;
     }
   }
+  // one PEM segment per warp 1..15 (warp 0 is busy with the RNG above); the
+  // segment's tok loads are issued before the barrier, under the RNG replay
+  const int j_first = warp - 1;
+  int uv[8];
+  static_assert(kSmallMns <= 8 * 32, "items per lane");
+#define RS_JOB_META(j)                                                               \
+  int e = 0;                                                                         \
+  for (int x = 0; x < n_est; ++x)                                                    \
+    if (__shfl_sync(kFull, jo, x) <= (j) && __shfl_sync(kFull, nj, x) > 0) e = x;    \
+  const int k = (j) - __shfl_sync(kFull, jo, e);                                     \
+  const int ne = __shfl_sync(kFull, nunp, e);                                        \
+  const int Le = __shfl_sync(kFull, L, e);                                           \
+  const int basee = __shfl_sync(kFull, base, e);                                     \
+  const int ole = __shfl_sync(kFull, ol, e);                                         \
+  const int t0 = k * (int)pm.mns - Le < 0 ? 0 : k * (int)pm.mns - Le;               \
+  const int t1 = (k + 1) * (int)pm.mns - Le < ne ? (k + 1) * (int)pm.mns - Le : ne;  \
+  const int nloc = t1 - t0;                                                          \
+  const int per = (nloc + 31) >> 5;                                                  \
+  const int x0 = lane * per;
+  if (warp > 0 && j_first < J) {
+    RS_JOB_META(j_first)
+    (void)ole;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) uv[i] = (i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
+  }
   __syncthreads();
   phase_mark(c, 7);
-  // one warp per PEM segment
-  for (int j = warp; j < J; j += kWarps) {
-    int e = 0;
-    for (int x = 0; x < n_est; ++x)
-      if (__shfl_sync(kFull, jo, x) <= j && __shfl_sync(kFull, nj, x) > 0) e = x;
-    const int k = j - __shfl_sync(kFull, jo, e);
-    const int ne = __shfl_sync(kFull, nunp, e);
-    const int Le = __shfl_sync(kFull, L, e);
-    const int basee = __shfl_sync(kFull, base, e);
-    const int ole = __shfl_sync(kFull, ol, e);
+  for (int j = j_first; warp > 0 && j < J; j += kWarps - 1) {
+    RS_JOB_META(j)
     const double ratio = S.est_ratio[e];
-    const long long t0l = (long long)k * pm.mns - Le, t1l = (long long)(k + 1) * pm.mns - Le;
-    const int t0 = t0l < 0 ? 0 : (int)t0l;
-    const int t1 = t1l < ne ? (int)t1l : ne;
-    const int nloc = t1 - t0;
     int* Uw = S.small.U[warp];
     {  // utok prefix of the segment: lane l owns items [l*per, l*per + per), per <= 8
-      // (nloc <= mns <= kSmallMns); all loads issue at once, one warp scan
-      static_assert(kSmallMns <= 8 * 32, "items per lane");
-      const int per = (nloc + 31) >> 5;
-      const int x0 = lane * per;
-      int uv[8];
+      // (nloc <= mns <= kSmallMns); one warp scan
+      if (j != j_first) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) uv[i] = (i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
+        for (int i = 0; i < 8; ++i) uv[i] = (i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
+      }
       int ls = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -394,6 +405,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     }
     __syncwarp();
   }
+#undef RS_JOB_META
   __syncthreads();
   phase_mark(c, 8);
   if (warp == 0 && lane < n_est) {  // ordered sums, relQuery by relQuery
@@ -402,7 +414,16 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       const int cnt = S.small.nterm[j];
       const double* tj = S.small.terms + j * kJobTerms;
       const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
-      for (int i = 0; i < cnt; ++i) total = __dadd_rn(total, i < kJobTerms ? tj[i] : spill[i]);
+      const int nsm = cnt < kJobTerms ? cnt : kJobTerms;
+      int i = 0;
+      for (; i + 8 <= nsm; i += 8) {  // loads of 8 terms in flight, then the dependent adds
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = tj[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) total = __dadd_rn(total, t[k]);
+      }
+      for (; i < cnt; ++i) total = __dadd_rn(total, i < kJobTerms ? tj[i] : spill[i]);
     }
     rq.prio[a] = total;
   }
