@@ -188,6 +188,43 @@ int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* fir
 int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t* prefilled,
                             int64_t* completion_iter, double* priority);
 
+/* ---------------------------------------------------------------------------
+ * Sharded pool (BASELINE config 5): one trace whose relQueries are
+ * owned round-robin by admission rank across `shards` shards.  Each shard
+ * keeps a full replica of the scheduler state and replays the same arranger
+ * and state advance; it re-estimates only the partially prefilled relQueries
+ * it owns and orders only its own waiting relQueries.  Once per scheduler
+ * iteration the shards allgather one record each (local waiting head + the
+ * priorities they computed) through peer memory inside the persistent kernel
+ * (paper_2601_11546_b200/csrc/shard.cuh).  Decisions are bit-identical to the
+ * unsharded engine.  Replaces nothing in the reference (which has no
+ * parallel engine); it is the multi-GPU form of run() (engine.py:466-475).
+ *
+ *   rank == -1 : every shard in this engine, one CTA per shard on `device`
+ *                (shards <= number of SMs); ready to step.
+ *   rank >= 0  : this engine is shard `rank` only (one process per GPU);
+ *                export rs_engine_mailbox() through rs_ipc_get_handle(),
+ *                map the peers' with rs_ipc_open_handle(), call
+ *                rs_engine_connect(), then step every shard with the same
+ *                max_iters (each launch waits for its peers every iteration).
+ * Status/log/ledger/request reads of any replica (t = 0) give the run's result.
+ * ------------------------------------------------------------------------- */
+int rs_engine_create_sharded(const rs_trace_view* trace, const rs_config* cfg, const rs_cost_model* world,
+                             const rs_cost_model* policy_model, const rs_pcg64_state* rng, int32_t device,
+                             int64_t log_capacity, int32_t shards, int32_t rank, rs_engine** out);
+
+/* Device pointer and size of a one-shard engine's mailbox (to export). */
+int rs_engine_mailbox(rs_engine* e, void** dptr, int64_t* bytes);
+
+/* peer_mailboxes[shards]: every shard's mailbox as addressable from this
+   engine's device (entry `rank` is ignored). */
+int rs_engine_connect(rs_engine* e, void* const* peer_mailboxes);
+
+/* CUDA IPC helpers (handle = 64 opaque bytes; cudaIpcMemHandle_t). */
+int rs_ipc_get_handle(void* dptr, uint8_t* handle);
+int rs_ipc_open_handle(const uint8_t* handle, int32_t device, void** dptr);
+int rs_ipc_close(void* dptr);
+
 /* Release all device memory of the engine. */
 void rs_engine_destroy(rs_engine* e);
 

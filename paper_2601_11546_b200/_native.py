@@ -61,6 +61,21 @@ def lib():
     L.rs_choice_sequence.restype = C.c_int
     L.rs_choice_sequence.argtypes = [C.POINTER(_abi.Pcg64State), C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_int32]
+    L.rs_engine_create_sharded.restype = C.c_int
+    L.rs_engine_create_sharded.argtypes = [C.POINTER(_abi.TraceView), C.POINTER(_abi.Config),
+                                           C.POINTER(_abi.CostModel), C.POINTER(_abi.CostModel),
+                                           C.POINTER(_abi.Pcg64State), C.c_int32, C.c_int64, C.c_int32,
+                                           C.c_int32, C.POINTER(C.c_void_p)]
+    L.rs_engine_mailbox.restype = C.c_int
+    L.rs_engine_mailbox.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+    L.rs_engine_connect.restype = C.c_int
+    L.rs_engine_connect.argtypes = [C.c_void_p, C.c_void_p]
+    L.rs_ipc_get_handle.restype = C.c_int
+    L.rs_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p]
+    L.rs_ipc_open_handle.restype = C.c_int
+    L.rs_ipc_open_handle.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.rs_ipc_close.restype = C.c_int
+    L.rs_ipc_close.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -70,6 +85,8 @@ EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_build_info", "rs_engine_create", "rs_engine_step", "rs_engine_status",
     "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_destroy",
     "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
+    "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
+    "rs_ipc_open_handle", "rs_ipc_close",
 )
 
 
@@ -98,18 +115,52 @@ class NativeEngine:
     """Owns an rs_engine handle (device SoA for one or more traces)."""
 
     def __init__(self, views, cfg: _abi.Config, world: _abi.CostModel, pol: _abi.CostModel, rngs,
-                 device: int, log_capacity: int):
+                 device: int, log_capacity: int, shards: int = 1, rank: int = -1):
+        """shards > 1: `views` is one trace, sharded (rank -1: every shard here, one CTA each;
+        rank >= 0: this process's shard, see connect())."""
         L = lib()
-        n = len(views)
-        arr_v = (_abi.TraceView * n)(*views)
-        arr_r = (_abi.Pcg64State * n)(*rngs)
         h = C.c_void_p()
         self._cfg, self._world, self._pol = cfg, world, pol
-        _check(L.rs_engine_create(arr_v, n, C.byref(cfg), C.byref(world), C.byref(pol), arr_r, device,
-                                  log_capacity, C.byref(h)))
+        if shards > 1:
+            assert len(views) == 1 and len(rngs) == 1
+            _check(L.rs_engine_create_sharded(C.byref(views[0]), C.byref(cfg), C.byref(world), C.byref(pol),
+                                              C.byref(rngs[0]), device, log_capacity, shards, rank,
+                                              C.byref(h)))
+            n = shards if rank < 0 else 1
+        else:
+            n = len(views)
+            arr_v = (_abi.TraceView * n)(*views)
+            arr_r = (_abi.Pcg64State * n)(*rngs)
+            _check(L.rs_engine_create(arr_v, n, C.byref(cfg), C.byref(world), C.byref(pol), arr_r, device,
+                                      log_capacity, C.byref(h)))
         self.h = h
         self.n = n
+        self.shards, self.rank = shards, rank
+        self.device = device
         self.log_capacity = log_capacity
+        self._opened: list[int] = []
+
+    # -- sharded pool, one shard per process (include/relserve.h) ----------
+    def mailbox_handle(self) -> bytes:
+        """CUDA IPC handle (64 bytes) of this shard's mailbox."""
+        p, nb = C.c_void_p(), C.c_int64()
+        _check(lib().rs_engine_mailbox(self.h, C.byref(p), C.byref(nb)))
+        buf = (C.c_uint8 * 64)()
+        _check(lib().rs_ipc_get_handle(p, buf))
+        return bytes(buf)
+
+    def connect(self, handles: list[bytes]):
+        """Map every peer's mailbox (handles[rank] is this shard's own) and connect."""
+        ptrs = (C.c_void_p * self.shards)()
+        for d, hd in enumerate(handles):
+            if d == self.rank:
+                continue
+            p = C.c_void_p()
+            buf = (C.c_uint8 * 64).from_buffer_copy(hd)
+            _check(lib().rs_ipc_open_handle(buf, self.device, C.byref(p)))
+            self._opened.append(p.value)
+            ptrs[d] = p
+        _check(lib().rs_engine_connect(self.h, ptrs))
 
     def step(self, max_iters: int, stream=None):
         _check(lib().rs_engine_step(self.h, int(max_iters), _stream_ptr(stream)))
@@ -152,6 +203,9 @@ class NativeEngine:
         if self.h:
             lib().rs_engine_destroy(self.h)
             self.h = None
+        for p in self._opened:
+            lib().rs_ipc_close(C.c_void_p(p))
+        self._opened = []
 
     def __del__(self):
         try:

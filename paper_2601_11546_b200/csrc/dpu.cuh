@@ -131,9 +131,11 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
   const int dper = 2 * Ssz - 1;
   // per-warp metadata: lane e holds relQuery e0 + e
   int a = 0, base = 0, nunp = 0, ol = 0, mcb = 0, L = 0, dcnt = 0, nj = 0;
+  bool own = false;  // sharded pool: only the owner estimates (shard.cuh); the RNG positions count every one
   if (lane < n_est) {
     const int ge = e0 + lane;
     a = ge < n_act ? c.act[ge] : S.new_lo + (ge - n_act);
+    own = T.shard_world == 1 || a % T.shard_world == T.shard_rank;
     const int off = rq.off[a];
     const int q = rq.q[a];
     base = off + q;
@@ -143,7 +145,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     L = rq.nrun[a];  // running rows = the live prefilled rows (prefilled summary)
     dcnt = nunp > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
     const int tot = nunp + L, mns = (int)pm.mns;  // 32-bit: rows per relQuery < 2^31
-    nj = tot > 0 ? (tot + mns - 1) / mns : 0;
+    nj = tot > 0 && own ? (tot + mns - 1) / mns : 0;
   }
   int jincl = warp_incl_scan(nj);
   {  // keep the prefix of relQueries whose segments fit the job buffers
@@ -159,7 +161,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
   const int doff = dincl - dcnt, jo = jincl - nj;
   const int D = __shfl_sync(kFull, dincl, 31), J = __shfl_sync(kFull, jincl, 31);
   {
-    const int nb_items = warp_sum(nunp), nb_samp = warp_sum(nunp > Ssz ? Ssz : nunp);
+    const int nb_items = warp_sum(own ? nunp : 0), nb_samp = warp_sum(own ? (nunp > Ssz ? Ssz : nunp) : 0);
     if (tid == 0) c.alg_bytes += 4LL * ((long long)nb_items + nb_samp);  // PEM items' tok + sampled tok
   }
   phase_mark(c, 5);
@@ -237,7 +239,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     if (rej) {  // replay sequentially: a rejection shifts every later draw
       if (lane == 0) ratios_sequential(P, T, S, e0, n_est, n_act);
     } else {
-      if (lane < n_est) {  // sample_cache_miss_ratio (prefix_cache.py:141-169)
+      if (lane < n_est && own) {  // sample_cache_miss_ratio (prefix_cache.py:141-169)
         const long long mh = cfg.block_size * (long long)mcb;  // exact utok = tok - B*m
         double ratio = 0.0;
         if (nunp > 0) {
@@ -298,8 +300,9 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       const int ae = __shfl_sync(kFull, a, e);
       const int Le = __shfl_sync(kFull, L, e);
       const int ole = __shfl_sync(kFull, ol, e);
+      const bool owne = __shfl_sync(kFull, (int)own, e);
       PrefixSummary ps{0, 0, 0};
-      if (Le > 0) {
+      if (Le > 0 && owne) {
         long long rs = 0, mx = 0;
         for (int j = lane; j < c.n_run; j += 32)
           if (c.run_rank[j] == ae) {
@@ -408,7 +411,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
 #undef RS_JOB_META
   __syncthreads();
   phase_mark(c, 8);
-  if (warp == 0 && lane < n_est) {  // ordered sums, relQuery by relQuery
+  if (warp == 0 && lane < n_est && own) {  // ordered sums, relQuery by relQuery
     double total = 0.0;
     for (int j = jo; j < jo + nj; ++j) {
       const int cnt = S.small.nterm[j];

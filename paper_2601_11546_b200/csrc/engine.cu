@@ -35,6 +35,7 @@
 #include "cache_model.cuh"
 #include "dpu.cuh"
 #include "engine_state.cuh"
+#include "shard.cuh"
 
 namespace rsd {
 
@@ -104,7 +105,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       int i0 = c.zptr;
       bool lead = true;
       for (int round = 0;; ++round) {
-        if (i0 >= T.R) break;
+        if (i0 >= T.nzl) break;
         if (round == kZScanRounds) {
           full = true;
           break;
@@ -112,7 +113,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         const int i = i0 + lane;
         bool gone = true, elig = false;
         int a = 0;
-        if (i < T.R) {
+        if (i < T.nzl) {
           a = rq.zl[i];
           const int q = rq.q[a], sz = rq.off[a + 1] - rq.off[a];
           // DPU policies: leaves the static order at its first prefill; sp/fcfs: when fully prefilled
@@ -122,7 +123,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         if (lead) {
           const unsigned keep = ~__ballot_sync(kFull, gone);
           if (keep == 0) {
-            zptr_new = i0 + 32 < T.R ? i0 + 32 : T.R;
+            zptr_new = i0 + 32 < T.nzl ? i0 + 32 : T.nzl;
           } else {
             zptr_new = i0 + __ffs(keep) - 1;
             lead = false;
@@ -136,10 +137,10 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         }
         i0 += 32;
       }
-      if (P.use_dpu) {  // partially prefilled relQueries with pending rows
+      if (P.use_dpu) {  // partially prefilled relQueries with pending rows (this shard's)
         for (int j = lane; j < c.n_act; j += 32) {
           const int a = c.act[j];
-          if (rq.q[a] < rq.off[a + 1] - rq.off[a]) {
+          if (rq.q[a] < rq.off[a + 1] - rq.off[a] && a % T.shard_world == T.shard_rank) {
             const unsigned long long k = dbits(rq.prio[a]);
             if (k < key || (k == key && a < idx)) {
               key = k;
@@ -163,7 +164,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       key = ~0ULL;
       idx = 0x7FFFFFFF;
       for (int a = tid; a < c.n_admitted; a += kThreads) {
-        if (rq.q[a] < rq.off[a + 1] - rq.off[a]) {
+        if (rq.q[a] < rq.off[a + 1] - rq.off[a] && a % T.shard_world == T.shard_rank) {
           ++w;
           const unsigned long long k = dbits(rq.prio[a]);
           if (k < key) {  // ranks visited in increasing order: strict < keeps the smallest rank
@@ -173,6 +174,9 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         }
       }
       block_count_argmin(w, key, idx, S.red);  // result is block-uniform in registers
+    }
+    if (T.shard_world > 1) {  // allgather of the shards' heads and priorities
+      if (!shard_exchange(T, S, key, idx)) return false;
     }
     head_l = c.n_wait > 0 && idx != 0x7FFFFFFF ? idx : -1;
     if (tid == 0) {
@@ -753,6 +757,10 @@ int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_by
 
 struct rs_engine {
   int device = 0;
+  int shard_world = 1, shard_rank = 0;  // sharded pool (rs_engine_create_sharded); rank -1: all shards here
+  ShardRec* mbox = nullptr;              // this engine's mailbox(es)
+  ShardRec** d_peers = nullptr;          // device array [world] of peer mailbox pointers
+  bool connected = true;                 // one-shard engines: peers' mailboxes known (rs_engine_connect)
   bool fast = true;  // every trace qualifies for engine_kernel<true>
   Params params{};
   std::vector<HostTrace> traces;
@@ -788,7 +796,8 @@ static int validate_config(const rs_config* cfg) {
 }
 
 static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_cost_model& pol,
-                       const rs_pcg64_state& rng, long long log_cap, HostTrace& h) {
+                       const rs_pcg64_state& rng, long long log_cap, HostTrace& h, int shard_world = 1,
+                       int shard_rank = 0) {
   h.pol = pol;
   const long long R = v.num_relqueries, N = v.num_requests;
   if (R < 0 || N < 0 || R > 0x7FFFFFF0LL || N > 0x7FFFFFF0LL) return fail(RS_EINVAL, "trace too large");
@@ -933,7 +942,12 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
         return b;
       };
       std::stable_sort(z.begin(), z.end(), [&](int x, int y) { return bits(x) < bits(y); });
-      for (long long i = 0; i < R; ++i) hv.zl[i] = z[i];
+      int nz = 0;  // a shard orders only the relQueries it owns (shard.cuh)
+      for (long long i = 0; i < R; ++i)
+        if (z[i] % shard_world == shard_rank) hv.zl[nz++] = z[i];
+      d.nzl = nz;
+      d.shard_world = shard_world;
+      d.shard_rank = shard_rank;
     }
     TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
     h.off.assign(off.begin(), off.end());
@@ -965,9 +979,23 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   return RS_OK;
 }
 
-int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_config* cfg,
-                     const rs_cost_model* world, const rs_cost_model* policy_model,
-                     const rs_pcg64_state* rng, int32_t device, int64_t log_capacity, rs_engine** out) {
+static int upload_traces(rs_engine* e) {
+  const int n = (int)e->traces.size();
+  std::vector<TraceDev> devs(n);
+  for (int t = 0; t < n; ++t) devs[t] = e->traces[t].dev;
+  if (!e->d_traces && cudaMalloc(&e->d_traces, sizeof(TraceDev) * n) != cudaSuccess)
+    return fail(RS_ECUDA, "trace table allocation failed");
+  if (cudaMemcpy(e->d_traces, devs.data(), sizeof(TraceDev) * n, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(RS_ECUDA, "trace table upload failed");
+  return RS_OK;
+}
+
+// shard_world == 1: independent traces.  shard_world > 1: every trace is a
+// replica of one trace; replica t is shard t when shard_rank == -1 (all
+// shards in this engine), else the single replica is shard `shard_rank`.
+static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_config* cfg,
+                       const rs_cost_model* world, const rs_cost_model* policy_model, const rs_pcg64_state* rng,
+                       int32_t device, int64_t log_capacity, int shard_world, int shard_rank, rs_engine** out) {
   *out = nullptr;
   if (n_traces <= 0) return fail(RS_EINVAL, "n_traces must be positive");
   int rc = validate_config(cfg);
@@ -975,15 +1003,36 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
   RS_CUDA(cudaSetDevice(device));
   rs_engine* e = new rs_engine();
   e->device = device;
+  e->shard_world = shard_world;
+  e->shard_rank = shard_rank;
   e->traces.resize(n_traces);
+  auto bail = [&](int code) {
+    std::string keep = g_err;
+    rs_engine_destroy(e);
+    g_err = keep;
+    return code;
+  };
   for (int t = 0; t < n_traces; ++t) {
-    rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t]);
-    if (rc) {
-      std::string keep = g_err;
-      rs_engine_destroy(e);
-      g_err = keep;
-      return rc;
+    const int srank = shard_world == 1 ? 0 : (shard_rank < 0 ? t : shard_rank);
+    rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t], shard_world, srank);
+    if (rc) return bail(rc);
+  }
+  if (shard_world > 1) {  // mailboxes (shard.cuh); zeroed: sequence numbers start at 1
+    const size_t mb = mailbox_bytes(shard_world);
+    const int n_mb = shard_rank < 0 ? shard_world : 1;
+    if (cudaMalloc(&e->mbox, mb * n_mb) != cudaSuccess || cudaMemset(e->mbox, 0, mb * n_mb) != cudaSuccess ||
+        cudaMalloc(&e->d_peers, sizeof(ShardRec*) * shard_world) != cudaSuccess)
+      return bail(fail(RS_ENOMEM, "mailbox allocation failed"));
+    std::vector<ShardRec*> peers(shard_world, nullptr);
+    for (int d = 0; d < shard_world; ++d)
+      peers[d] = shard_rank < 0 ? (ShardRec*)((char*)e->mbox + mb * d) : (d == shard_rank ? e->mbox : nullptr);
+    if (cudaMemcpy(e->d_peers, peers.data(), sizeof(ShardRec*) * shard_world, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(RS_ECUDA, "mailbox table upload failed"));
+    for (int t = 0; t < n_traces; ++t) {
+      e->traces[t].dev.self_mbox = shard_rank < 0 ? peers[t] : e->mbox;
+      e->traces[t].dev.peers = e->d_peers;
     }
+    e->connected = shard_rank < 0;
   }
   // shared memory: the control block etc., plus the relQuery table of every
   // trace whose table fits next to it (the others read theirs from HBM)
@@ -996,13 +1045,7 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
     h.dev.rq_in_smem = base + rb <= (size_t)max_optin;
     if (h.dev.rq_in_smem) need = std::max(need, base + rb);
   }
-  std::vector<TraceDev> devs(n_traces);
-  for (int t = 0; t < n_traces; ++t) devs[t] = e->traces[t].dev;
-  if (cudaMalloc(&e->d_traces, sizeof(TraceDev) * n_traces) != cudaSuccess ||
-      cudaMemcpy(e->d_traces, devs.data(), sizeof(TraceDev) * n_traces, cudaMemcpyHostToDevice) != cudaSuccess) {
-    rs_engine_destroy(e);
-    return fail(RS_ECUDA, "trace table upload failed");
-  }
+  if ((rc = upload_traces(e))) return bail(rc);
   Params& p = e->params;
   p.traces = e->d_traces;
   p.cfg = *cfg;
@@ -1018,16 +1061,76 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
   cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce == cudaSuccess)
     ce = cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  if (ce != cudaSuccess) {
-    rs_engine_destroy(e);
-    return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce));
-  }
+  if (ce != cudaSuccess) return bail(fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
   *out = e;
+  return RS_OK;
+}
+
+int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_config* cfg,
+                     const rs_cost_model* world, const rs_cost_model* policy_model,
+                     const rs_pcg64_state* rng, int32_t device, int64_t log_capacity, rs_engine** out) {
+  return create_impl(traces, n_traces, cfg, world, policy_model, rng, device, log_capacity, 1, 0, out);
+}
+
+int rs_engine_create_sharded(const rs_trace_view* trace, const rs_config* cfg, const rs_cost_model* world,
+                             const rs_cost_model* policy_model, const rs_pcg64_state* rng, int32_t device,
+                             int64_t log_capacity, int32_t shards, int32_t rank, rs_engine** out) {
+  *out = nullptr;
+  if (shards < 1 || shards > 32) return fail(RS_EINVAL, "shards must be in [1, 32]");
+  if (rank < -1 || rank >= shards) return fail(RS_EINVAL, "rank must be -1 or in [0, shards)");
+  int n_sm = 0;
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (rank < 0 && shards > n_sm) return fail(RS_EINVAL, "all-shards-here mode needs one SM per shard");
+  const int n = rank < 0 ? shards : 1;
+  std::vector<rs_trace_view> views(n, *trace);
+  std::vector<rs_pcg64_state> rngs(n, *rng);
+  return create_impl(views.data(), n, cfg, world, policy_model, rngs.data(), device, log_capacity, shards,
+                     shards == 1 ? 0 : rank, out);
+}
+
+int rs_engine_mailbox(rs_engine* e, void** dptr, int64_t* bytes) {
+  if (!e || e->shard_world < 2 || e->shard_rank < 0) return fail(RS_EINVAL, "not a one-shard sharded engine");
+  *dptr = e->mbox;
+  *bytes = (int64_t)mailbox_bytes(e->shard_world);
+  return RS_OK;
+}
+
+int rs_engine_connect(rs_engine* e, void* const* peer_mailboxes) {
+  if (!e || e->shard_world < 2 || e->shard_rank < 0) return fail(RS_EINVAL, "not a one-shard sharded engine");
+  RS_CUDA(cudaSetDevice(e->device));
+  std::vector<ShardRec*> peers(e->shard_world);
+  for (int d = 0; d < e->shard_world; ++d) {
+    peers[d] = d == e->shard_rank ? e->mbox : (ShardRec*)peer_mailboxes[d];
+    if (!peers[d]) return fail(RS_EINVAL, "null peer mailbox");
+  }
+  RS_CUDA(cudaMemcpy(e->d_peers, peers.data(), sizeof(ShardRec*) * e->shard_world, cudaMemcpyHostToDevice));
+  e->connected = true;
+  return RS_OK;
+}
+
+int rs_ipc_get_handle(void* dptr, uint8_t* handle) {
+  cudaIpcMemHandle_t h;
+  RS_CUDA(cudaIpcGetMemHandle(&h, dptr));
+  memcpy(handle, &h, sizeof h);
+  return RS_OK;
+}
+
+int rs_ipc_open_handle(const uint8_t* handle, int32_t device, void** dptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  RS_CUDA(cudaSetDevice(device));
+  RS_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RS_OK;
+}
+
+int rs_ipc_close(void* dptr) {
+  RS_CUDA(cudaIpcCloseMemHandle(dptr));
   return RS_OK;
 }
 
 int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
   if (!e) return fail(RS_EINVAL, "null engine");
+  if (e->shard_world > 1 && !e->connected) return fail(RS_EINVAL, "sharded engine not connected to its peers");
   RS_CUDA(cudaSetDevice(e->device));
   long long cap = e->params.cfg.log_decisions ? e->traces[0].dev.log_cap : max_iters;
   if (e->params.cfg.log_decisions && cap > 0 && max_iters > cap) max_iters = cap;
@@ -1142,6 +1245,8 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
 void rs_engine_destroy(rs_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
+  if (e->mbox) cudaFree(e->mbox);
+  if (e->d_peers) cudaFree(e->d_peers);
   for (auto& h : e->traces)
     for (void* p : h.allocs) cudaFree(p);
   if (e->d_traces) cudaFree(e->d_traces);

@@ -22,6 +22,8 @@
 
 namespace rsd {
 
+struct ShardRec;  // shard.cuh
+
 constexpr int kMaxRun = 1024;   // device limit on max_num_seqs
 constexpr int kMaxAct = 1024;   // partially-prefilled live relQueries
 constexpr int kMaxCC = 256;     // tail-less resident chains
@@ -142,6 +144,11 @@ struct TraceDev {
   const double* fsprio;   // [R] first-sight priority (static: no prefilled row, cold chain, ratio 1.0)
   const long long* fs_doff;  // [R+1] prefix of first-sight draw counts (2S-1 per relQuery larger than S)
   int fast;                  // engine_kernel<true> applies (see host)
+  int nzl;                   // entries of rq.zl (this shard's relQueries)
+  int shard_world, shard_rank;  // sharded pool: relQuery a is owned by shard a % world (1, 0: unsharded)
+  int pad1;
+  ShardRec* self_mbox;       // this shard's mailbox ShardRec[world][2] (shard.cuh)
+  ShardRec* const* peers;    // [world] every shard's mailbox, as addressable from this device
   rs_iter_record* log;
   long long log_cap;
   Ctl* ctl;

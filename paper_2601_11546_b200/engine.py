@@ -182,7 +182,12 @@ class Engine:
         *,
         device: int = 0,
         stream=None,
+        shards: int = 1,
+        shard_rank: int = -1,
     ):
+        """shards > 1 runs the sharded pool (include/relserve.h rs_engine_create_sharded):
+        shard_rank -1 puts every shard on `device` (one CTA each); shard_rank >= 0 makes this
+        engine one shard of a multi-process group (call connect_shards before run/step)."""
         if policy not in POLICIES:
             raise ValueError(f"unknown policy {policy!r}; choose from {POLICIES}")
         self.trace = trace
@@ -206,14 +211,25 @@ class Engine:
         self._native = _native.NativeEngine(
             [self._m.view], _marshal.make_config(c, policy), _marshal.make_model(world_model),
             _marshal.make_model(self.policy_model), [_marshal.dpu_rng_state(seed)], device,
-            log_capacity=self.chunk_iterations if c.log_decisions else 0,
+            log_capacity=self.chunk_iterations if c.log_decisions else 0, shards=shards, rank=shard_rank,
         )
+        self.shards, self.shard_rank = shards, shard_rank
         self.iteration = 0
         self.clock = 0.0
         self.kv_reserved = 0
         self._records: list[np.ndarray] = []
         self._status = None
         self.result: RunResult | None = None
+
+    # -- sharded pool across processes ----------------------------------------
+
+    def mailbox_handle(self) -> bytes:
+        """CUDA IPC handle of this shard's mailbox (shard_rank >= 0)."""
+        return self._native.mailbox_handle()
+
+    def connect_shards(self, handles: list[bytes]) -> None:
+        """handles[r] = shard r's mailbox_handle(), gathered from every process."""
+        self._native.connect(handles)
 
     # -- device loop ---------------------------------------------------------
 
