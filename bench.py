@@ -58,7 +58,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--iters-per-step", type=int, default=250)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["2", "3", "4"], default="2")
+    ap.add_argument("--config", choices=["2", "3", "4", "5"], default="2")
+    ap.add_argument("--shards", type=int, default=None,
+                    help="config 5 on one GPU: shards as CTAs of one launch (default 8); under torchrun "
+                         "every rank is one shard")
     ap.add_argument("--traces-per-gpu", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -74,10 +77,15 @@ def workload(cfg_id: str, seed: int):
         trace = generate_trace(TraceConfig(num_relqueries=1000, size_range=(1000, 1000), rate=1e6, seed=seed))
         world = world_preset("opt-13b-like")
         name = "config2: 1000 relQ x 1000 rows, opt-13b-like (Llama-2-13B), relserve"
-    else:
+    elif cfg_id == "3":
         trace = generate_heavy_tail_trace(num_relqueries=5000, size_range=(1, 399), rate=1e6, seed=seed)
         world = world_preset("llama-70b-like")
         name = "config3: 5000 relQ x U[1,399] heavy-tailed outputs, llama-70b-like (Llama-2-70B), relserve"
+    else:
+        trace = generate_heavy_tail_trace(num_relqueries=40000, size_range=(1, 399), rate=1e6, seed=seed)
+        world = world_preset("llama-70b-like")
+        name = ("config5: one pool of 40000 relQ x U[1,399] (8e6 requests) heavy-tailed outputs, "
+                "llama-70b-like (Llama-2-70B), relserve, relQueries sharded round-robin")
     return trace, world, EngineConfig(), name
 
 
@@ -186,15 +194,24 @@ def run_ours(args, ws, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    trace, world, cfg, wname = workload(args.config, seed=rank)
+    pool = args.config == "5"  # one trace sharded over the ranks (or over CTAs on one GPU)
+    trace, world, cfg, wname = workload(args.config, seed=0 if pool else rank)
     I = args.iters_per_step
     stream = torch.cuda.current_stream(dev)
+    if pool:
+        shards, srank = (ws, rank) if ws > 1 else (args.shards or 8, -1)
+    else:
+        shards, srank = 1, -1
 
     # ---- device-resident timing (inputs already in HBM)
     m = _marshal.marshal_trace(trace, cfg.block_size, "relserve", world, None)
     ne = NativeEngine([m.view], _marshal.make_config(cfg, "relserve"), _marshal.make_model(world),
                       _marshal.make_model(world), [_marshal.dpu_rng_state(0)], local,
-                      log_capacity=I * (args.steps + args.warmup + 1) + WINDOW_START)
+                      log_capacity=I * (args.steps + args.warmup + 1) + WINDOW_START, shards=shards, rank=srank)
+    if pool and ws > 1:
+        from paper_2601_11546_b200 import sharded
+
+        ne.connect(sharded.exchange_handles(ne.mailbox_handle()))
     ne.step(WINDOW_START, stream)
     st = ne.status(stream)[0]
     assert st.status == _abi.RS_RUNNING and st.iterations == WINDOW_START, (st.status, st.iterations)
@@ -239,7 +256,8 @@ def run_ours(args, ws, rank, local):
     ne.close()
     t_ms = sum(step_ms)
     t_max = max_over_ranks(t_ms, ws, dev)
-    total_iters = sum_over_ranks(float(iters), ws, dev)
+    # independent traces: every rank's iterations count; one sharded pool: its iterations once
+    total_iters = float(iters) if pool else sum_over_ranks(float(iters), ws, dev)
     value = total_iters / (t_max / 1e3)
     c = trace.columns()
     per_launch_bytes = alg_window / args.steps
@@ -252,7 +270,12 @@ def run_ours(args, ws, rank, local):
     if not args.no_e2e:
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        eng = Engine(trace, "relserve", world, cfg, seed=0, device=local, stream=stream)
+        eng = Engine(trace, "relserve", world, cfg, seed=0, device=local, stream=stream, shards=shards,
+                     shard_rank=srank)
+        if pool and ws > 1:
+            from paper_2601_11546_b200 import sharded
+
+            sharded.connect(eng)
         eng.chunk_iterations = I
         st0 = eng.step(WINDOW_START)
         for _ in range(args.steps):
@@ -266,7 +289,7 @@ def run_ours(args, ws, rank, local):
         d2h_step = I * 96 + 128
         d2h_final = c.num_requests * (4 + 1 + 8 + 8) + c.num_relqueries * 32
         wall_max = max_over_ranks(wall, ws, dev)
-        e2e_total = sum_over_ranks(float(e_iters), ws, dev)
+        e2e_total = float(e_iters) if pool else sum_over_ranks(float(e_iters), ws, dev)
         e2e = {"value": e2e_total / wall_max, "unit": "iters/s",
                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / args.steps),
                "iterations": int(e_iters), "wall_s": wall_max,
@@ -286,14 +309,16 @@ def run_ours(args, ws, rank, local):
             "warmup": args.warmup,
             "ms_per_step": t_max / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if pool else "weak",
             "vs_baseline": None,
             "dtype": "f64+int32",
             "data": "synthetic (relsim generate_trace, count-identical to the reference generator)",
             "config": {"workload": wname, "iters_per_step": I, "window_start_iteration": WINDOW_START,
+                       "shards": shards, "shard_mode": ("one per GPU (NVLink P2P mailboxes)" if pool and ws > 1
+                                                        else "CTAs of one launch on one GPU" if pool else None),
                        "pending_requests_start": pending0, "pending_requests_end": pending_end,
                        "l2": "256 MiB buffer written between timed steps (outside the events)",
-                       "traces_per_gpu": 1},
+                       "traces_per_gpu": 1 if not pool else None},
             "iterations_timed": int(total_iters),
             "e2e": e2e,
             "gpu_launches": args.steps,
@@ -319,7 +344,7 @@ def cpu_baseline(args, trace, world, cfg, iters=None):
 
     from oracle import oracle
 
-    iters = iters or args.cpu_iters
+    iters = iters or (args.cpu_iters if args.config in ("2", "3") else min(args.cpu_iters, 1000))
     c2 = replace(cfg, iteration_limit=WINDOW_START + iters)
     t0 = time.perf_counter()
     r = oracle.run(trace, "relserve", world, c2, None, 0)

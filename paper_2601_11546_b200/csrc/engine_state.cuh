@@ -182,6 +182,8 @@ struct Shared {
   long long utok_sum;
   double m_plus, m_minus;
   int dmin_slot, n_est;
+  unsigned long long sh_key[32];  // sharded pool: the shards' waiting heads of this iteration
+  int sh_idx[32];
   int n_dist, act_dirty, rrq_dirty;
   int sorted_dist[kMaxRun];
   int cand_tok[kMaxRun];  // staged candidate prefill rows (tok, out)
