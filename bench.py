@@ -269,6 +269,9 @@ def run_ours(args, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         torch.cuda.synchronize(dev)
+        import gc
+
+        gc.collect()
         t0 = time.perf_counter()
         eng = Engine(trace, "relserve", world, cfg, seed=0, device=local, stream=stream, shards=shards,
                      shard_rank=srank)
@@ -277,12 +280,16 @@ def run_ours(args, ws, rank, local):
 
             sharded.connect(eng)
         eng.chunk_iterations = I
+        t1 = time.perf_counter()
         st0 = eng.step(WINDOW_START)
         for _ in range(args.steps):
             eng.step(I)
+        t2 = time.perf_counter()
         res = eng._collect(0.0)
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t0
+        e2e_parts = {"create_ms": 1e3 * (t1 - t0), "steps_ms": 1e3 * (t2 - t1),
+                     "collect_ms": 1e3 * (time.perf_counter() - t2)}
         e_iters = eng.iteration
         eng.close()
         h2d = sum(v.nbytes for v in m.arrays.values() if v is not None)
@@ -292,7 +299,7 @@ def run_ours(args, ws, rank, local):
         e2e_total = float(e_iters) if pool else sum_over_ranks(float(e_iters), ws, dev)
         e2e = {"value": e2e_total / wall_max, "unit": "iters/s",
                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / args.steps),
-               "iterations": int(e_iters), "wall_s": wall_max,
+               "iterations": int(e_iters), "wall_s": wall_max, "breakdown_ms": e2e_parts,
                "includes": "trace upload, iterations 0..window end (incl. first-sight DPU), per-step record readback, final ledger/request readback"}
 
     out = None

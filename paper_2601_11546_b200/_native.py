@@ -90,8 +90,13 @@ EXPORTED_SYMBOLS = (
 )
 
 
+_clock_khz: dict[int, int] = {}
+
+
 def device_clock_khz(device: int = 0) -> int:
-    return int(lib().rs_device_clock_khz(device))
+    if device not in _clock_khz:  # the attribute query costs milliseconds
+        _clock_khz[device] = int(lib().rs_device_clock_khz(device))
+    return _clock_khz[device]
 
 
 def _check(rc: int):

@@ -25,6 +25,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstddef>
 #include <cstdlib>
 #include <numeric>
@@ -715,6 +716,18 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// RS_TIMING=1 in the environment: host-side phase times of engine creation on stderr
+struct PhaseClock {
+  bool on = getenv("RS_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rs] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 #define RS_CUDA(call)                                                                     \
   do {                                                                                    \
     cudaError_t _e = (call);                                                              \
@@ -728,20 +741,42 @@ struct HostTrace {
   std::vector<int> off;                // rank-ordered row offsets
   std::vector<int> rank_of;     // trace index -> rank
   std::vector<int> order;       // rank -> trace index
-  std::vector<long long> row_src;  // rank-ordered row -> trace-order row
+  std::vector<long long> row_src;  // rank-ordered row -> trace-order row (empty: identity)
   std::vector<void*> allocs;
   long long bytes = 0;
   long long log_read = 0;
+  // one device arena per trace (a cudaMalloc per buffer costs more than the upload itself)
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
 };
+
+// Reserve the trace's arena: every dalloc below carves from it (256-byte aligned).
+int arena_reserve(HostTrace& h, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  h.allocs.push_back(q);
+  h.arena = (char*)q;
+  h.arena_cap = bytes;
+  h.arena_used = 0;
+  return RS_OK;
+}
 
 template <typename T>
 int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_byte = -1) {
   if (n == 0) n = 1;
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, n * sizeof(T));
-  if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-  h.allocs.push_back(q);
+  const size_t nb = (n * sizeof(T) + 255) & ~(size_t)255;
+  if (h.arena && h.arena_used + nb <= h.arena_cap) {
+    q = h.arena + h.arena_used;
+    h.arena_used += nb;
+  } else {
+    cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+    if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    h.allocs.push_back(q);
+  }
   h.bytes += (long long)(n * sizeof(T));
+  cudaError_t e = cudaSuccess;
   if (src) {
     e = cudaMemcpy(q, src, n * sizeof(T), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -799,6 +834,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
                        const rs_pcg64_state& rng, long long log_cap, HostTrace& h, int shard_world = 1,
                        int shard_rank = 0) {
   h.pol = pol;
+  PhaseClock pc;
   const long long R = v.num_relqueries, N = v.num_requests;
   if (R < 0 || N < 0 || R > 0x7FFFFFF0LL || N > 0x7FFFFFF0LL) return fail(RS_EINVAL, "trace too large");
   if (v.row_off[0] != 0 || v.row_off[R] != N) return fail(RS_EINVAL, "row_off must span [0, N]");
@@ -816,10 +852,16 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   std::vector<double> arrival(R), sprio(R, 0.0);
   std::vector<int> off(R + 1), ol(R), chain(R);
   std::vector<long long> relid(R);
-  std::vector<int> tok(N), out(N);
-  h.row_src.resize(N);
+  // admission order == trace order (the common case: entries sorted by
+  // arrival, then rel_id): rows are uploaded straight from the caller's arrays
+  bool ident = true;
+  for (long long a = 0; a < R && ident; ++a) ident = h.order[a] == a;
+  std::vector<int> tok_buf(ident ? 0 : N), out_buf(ident ? 0 : N);
+  int* tok = ident ? const_cast<int*>(v.tok) : tok_buf.data();
+  int* out = ident ? const_cast<int*>(v.out) : out_buf.data();
+  if (!ident) h.row_src.resize(N);
   int max_size = 1;
-  long long max_nb = 0;
+  long long max_nb = 0, max_tok_all = 0;
   long long k = 0;
   off[0] = 0;
   for (long long a = 0; a < R; ++a) {
@@ -835,24 +877,44 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     if (hi - lo > max_size) max_size = (int)(hi - lo);
     if (dpu && cfg->sample_size > 200 && hi - lo > 10000)
       return fail(RS_EUNSUPPORTED, "Generator.choice tail-shuffle branch is not replayed");
-    for (long long r = lo; r < hi; ++r) {
-      tok[k] = v.tok[r];
-      out[k] = v.out[r];
-      h.row_src[k] = r;
-      if (tok[k] <= 0) return fail(RS_EINVAL, "request tokens must be non-empty");
-      if (out[k] < 1 || out[k] > ol[a]) return fail(RS_EINVAL, "actual_output_len out of range");
-      if ((long long)tok[k] + ol[a] > cfg->cap) {
-        char msg[200];
-        snprintf(msg, sizeof msg, "request %lld/%lld needs %lld KV tokens > cap %lld", (long long)relid[a],
-                 (long long)(r - lo), (long long)tok[k] + ol[a], (long long)cfg->cap);
-        return fail(RS_EINFEASIBLE, msg);
+    // rows: bulk copy, then range checks on per-relQuery min / max (the
+    // per-row scan below runs only to name the offending row)
+    const long long n = hi - lo;
+    if (n > 0) {
+      if (!ident) {
+        memcpy(&tok[k], v.tok + lo, n * sizeof(int));
+        memcpy(&out[k], v.out + lo, n * sizeof(int));
+        std::iota(h.row_src.begin() + k, h.row_src.begin() + k + n, lo);
       }
-      if ((long long)tok[k] + ol[a] >= (1LL << 20))
-        return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
-      const long long nb = tok[k] / cfg->block_size;
-      if (nb < chain[a]) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
+      int tmin = tok[k], tmax = tok[k], omin = out[k], omax = out[k];
+      for (long long i = k; i < k + n; ++i) {
+        tmin = std::min(tmin, tok[i]);
+        tmax = std::max(tmax, tok[i]);
+        omin = std::min(omin, out[i]);
+        omax = std::max(omax, out[i]);
+      }
+      const long long lim_lo = (long long)chain[a] * cfg->block_size;  // nb >= chain  <=>  tok >= chain * B
+      if (tmin <= 0 || omin < 1 || omax > ol[a] || (long long)tmax + ol[a] > cfg->cap ||
+          (long long)tmax + ol[a] >= (1LL << 20) || tmin < lim_lo) {
+        for (long long r = lo; r < hi; ++r) {
+          const long long tk = v.tok[r], ou = v.out[r];
+          if (tk <= 0) return fail(RS_EINVAL, "request tokens must be non-empty");
+          if (ou < 1 || ou > ol[a]) return fail(RS_EINVAL, "actual_output_len out of range");
+          if (tk + ol[a] > cfg->cap) {
+            char msg[200];
+            snprintf(msg, sizeof msg, "request %lld/%lld needs %lld KV tokens > cap %lld", (long long)relid[a],
+                     (long long)(r - lo), tk + ol[a], (long long)cfg->cap);
+            return fail(RS_EINFEASIBLE, msg);
+          }
+          if (tk + ol[a] >= (1LL << 20))
+            return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
+          if (tk < lim_lo) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
+        }
+      }
+      const long long nb = tmax / cfg->block_size;
       if (nb > max_nb) max_nb = nb;
-      ++k;
+      if (tmax > max_tok_all) max_tok_all = tmax;
+      k += n;
     }
     off[a + 1] = (int)k;
   }
@@ -863,8 +925,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   d.N = (int)N;
   d.max_size = max_size;
   {
-    long long max_tok = 0;
-    for (long long i = 0; i < N; ++i) max_tok = std::max<long long>(max_tok, tok[i]);
+    const long long max_tok = max_tok_all;
     d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
     // engine_kernel<true> (no general DPU path) needs count-only PEM segments,
     // mns and sample size within the warp fast path, and every relQuery's
@@ -875,8 +936,25 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   int rc;
 #define TRY(x) \
   if ((rc = (x))) return rc
-  TRY(dalloc(h, (int**)&d.tok, N, tok.data()));
-  TRY(dalloc(h, (int**)&d.out, N, out.data()));
+  {  // arena: an upper bound of every buffer below (+256 B alignment slack each)
+    long long fifo_cap = 1;
+    while (fifo_cap < cfg->capacity_blocks + kMaxRun + 2) fifo_cap <<= 1;
+    long long lc = 0;
+    if (log_cap > 0) {
+      lc = 1;
+      while (lc < log_cap) lc <<= 1;
+    }
+    const size_t need = 16 * (size_t)N + 24 * (size_t)R + 8 * (size_t)kMaxJobs * (kSmallMns + 1) +
+                        8 * (size_t)(R + 1) + 8 * (size_t)R + 4 * (size_t)(R + 1) + 4 * (size_t)R +
+                        rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
+                        (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
+                        32 * 256;
+    pc.mark("host rows");
+    TRY(arena_reserve(h, need));
+  }
+  pc.mark("host rows + arena");
+  TRY(dalloc(h, (int**)&d.tok, N, tok));
+  TRY(dalloc(h, (int**)&d.out, N, out));
   std::vector<double> nanv(R, NAN);
   TRY(dalloc(h, &d.fps, R, nanv.data()));
   TRY(dalloc(h, &d.lpe, R, nanv.data()));
@@ -885,6 +963,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
   TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
   {
+    pc.mark("row uploads");
     // first sight (dpu.cuh first_sight): draw-count prefix on the host, the
     // static PEM of every relQuery by one wide kernel
     std::vector<long long> fsd(R + 1, 0);
@@ -906,6 +985,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first_sight_kernel: ") + cudaGetErrorString(ke));
     }
   }
+  pc.mark("first-sight kernel");
   // relQuery table (rq_carve layout), uploaded as one block
   {
     // rank of each rel_id among all rel_ids: the Delta projection's sort key
@@ -952,6 +1032,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
     h.off.assign(off.begin(), off.end());
   }
+  pc.mark("relQuery table");
   d.fifo_cap = 1;  // >= capacity + kMaxRun + 2: batched pushes precede evictions
   while (d.fifo_cap < cfg->capacity_blocks + kMaxRun + 2) d.fifo_cap <<= 1;
   TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
@@ -968,6 +1049,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     while (d.log_cap < log_cap) d.log_cap <<= 1;
     TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
   }
+  pc.mark("fifo/jump/log");
   Ctl* ctl = (Ctl*)calloc(1, sizeof(Ctl));
   if (!ctl) return fail(RS_ENOMEM, "host alloc");
   ctl->status = RS_RUNNING;
@@ -1000,7 +1082,9 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   if (n_traces <= 0) return fail(RS_EINVAL, "n_traces must be positive");
   int rc = validate_config(cfg);
   if (rc) return rc;
+  PhaseClock pc;
   RS_CUDA(cudaSetDevice(device));
+  pc.mark("cudaSetDevice");
   rs_engine* e = new rs_engine();
   e->device = device;
   e->shard_world = shard_world;
@@ -1034,6 +1118,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
     }
     e->connected = shard_rank < 0;
   }
+  pc.mark("traces built");
   // shared memory: the control block etc., plus the relQuery table of every
   // trace whose table fits next to it (the others read theirs from HBM)
   const size_t base = (sizeof(Shared) + 15) & ~(size_t)15;
@@ -1046,6 +1131,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
     if (h.dev.rq_in_smem) need = std::max(need, base + rb);
   }
   if ((rc = upload_traces(e))) return bail(rc);
+  pc.mark("trace table");
   Params& p = e->params;
   p.traces = e->d_traces;
   p.cfg = *cfg;
@@ -1062,6 +1148,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   if (ce == cudaSuccess)
     ce = cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce != cudaSuccess) return bail(fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
+  pc.mark("kernel attributes");
   *out = e;
   return RS_OK;
 }
@@ -1227,12 +1314,17 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
   if (N && completion_iter) RS_CUDA(cudaMemcpy(comp.data(), h.dev.comp, N * 4, cudaMemcpyDeviceToHost));
   if (prefilled || priority) RS_CUDA(cudaMemcpy(tab.data(), h.dev.rq_global, tab.size(), cudaMemcpyDeviceToHost));
   const RqView v = rq_carve(tab.data(), R);
+  if (h.row_src.empty() && !generated && !prefilled && !priority) {  // identity order, completion only
+    for (int k = 0; k < N; ++k) completion_iter[k] = comp[k];
+    return RS_OK;
+  }
   for (int a = 0; a < R; ++a) {
     const int lo = h.off[a], hi = h.off[a + 1];
     const int qa = (prefilled || priority) ? v.q[a] : 0;
     const double pa = priority ? v.prio[a] : 0.0;
+    const bool ident = h.row_src.empty();
     for (int k = lo; k < hi; ++k) {
-      const long long src = h.row_src[k];
+      const long long src = ident ? k : h.row_src[k];
       if (generated) generated[src] = gen[k];
       if (prefilled) prefilled[src] = (k - lo) < qa;
       if (completion_iter) completion_iter[src] = comp[k];

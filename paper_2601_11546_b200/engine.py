@@ -149,6 +149,50 @@ _DPU_PHASES = (1, 5, 6, 7, 8, 15, 16, 17, 18)
 _ABA_PHASES = (2, 3, 11, 12)
 
 
+class _DecisionLog(list):
+    """RunResult.decision_log (engine.py:64-74, 419-433): a list of
+    DecisionLogEntry built from the device records on first use."""
+
+    def __init__(self, recs: np.ndarray):
+        super().__init__()
+        self._recs = recs
+
+    def _fill(self):
+        recs, self._recs = self._recs, None
+        if recs is None or not len(recs):
+            return
+        cols = [recs[k].tolist() for k in ("iteration", "clock", "kase", "m_plus", "m_minus", "delta_plus",
+                                           "delta_minus", "delta_total", "action")]
+        nan = math.isnan
+        out = []
+        for it, clk, ks, mp, mm, dp, dm, dt, ac in zip(*cols):
+            proj = not nan(dp)
+            out.append(DecisionLogEntry(
+                it, clk, _abi.CASES[ks], None if nan(mp) else mp, None if nan(mm) else mm,
+                dp if proj else None, dm if proj else None, dt if proj else None, _abi.ACTIONS[ac]))
+        list.extend(self, out)
+
+    def _ready(self):
+        if self._recs is not None:
+            self._fill()
+
+
+for _name in ("__len__", "__iter__", "__getitem__", "__contains__", "__eq__", "__repr__", "__reversed__",
+              "__bool__", "index", "count", "copy", "__add__", "__mul__"):
+    if hasattr(list, _name):
+        def _wrap(name=_name):
+            base = getattr(list, name)
+
+            def f(self, *a, **k):
+                self._ready()
+                return base(self, *a, **k)
+
+            f.__name__ = name
+            return f
+
+        setattr(_DecisionLog, _name, _wrap())
+
+
 _ERRORS = {
     _abi.RS_EINVAL: ValueError,
     _abi.RS_EINFEASIBLE: InfeasibleRequestError,
@@ -281,16 +325,7 @@ class Engine:
             ledgers[rid[i]] = TimestampLedger(av[i], _opt(fv[i]), _opt(lv[i]), _opt(dv[i]))
         recs = (np.concatenate(self._records) if self._records
                 else np.zeros(0, _abi.ITER_RECORD_DTYPE))
-        log = []
-        if self.config.log_decisions and len(recs):
-            cols = {k: recs[k].tolist() for k in ("iteration", "clock", "kase", "m_plus", "m_minus",
-                                                  "delta_plus", "delta_minus", "delta_total", "action")}
-            nan = math.isnan
-            for it, clk, ks, mp, mm, dp, dm, dt, ac in zip(*cols.values()):
-                proj = not nan(dp)
-                log.append(DecisionLogEntry(
-                    it, clk, _abi.CASES[ks], None if nan(mp) else mp, None if nan(mm) else mm,
-                    dp if proj else None, dm if proj else None, dt if proj else None, _abi.ACTIONS[ac]))
+        log = _DecisionLog(recs if self.config.log_decisions else recs[:0])
         self._requests_state = None
         if self.trace.materialized:  # reference semantics: the run mutates the Request objects
             gen, pre, _, prio = self.requests_state
