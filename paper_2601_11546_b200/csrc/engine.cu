@@ -141,7 +141,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       if (P.use_dpu) {  // partially prefilled relQueries with pending rows (this shard's)
         for (int j = lane; j < c.n_act; j += 32) {
           const int a = c.act[j];
-          if (rq.q[a] < rq.off[a + 1] - rq.off[a] && a % T.shard_world == T.shard_rank) {
+          if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
             const unsigned long long k = dbits(rq.prio[a]);
             if (k < key || (k == key && a < idx)) {
               key = k;
@@ -165,7 +165,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       key = ~0ULL;
       idx = 0x7FFFFFFF;
       for (int a = tid; a < c.n_admitted; a += kThreads) {
-        if (rq.q[a] < rq.off[a + 1] - rq.off[a] && a % T.shard_world == T.shard_rank) {
+        if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
           ++w;
           const unsigned long long k = dbits(rq.prio[a]);
           if (k < key) {  // ranks visited in increasing order: strict < keeps the smallest rank
