@@ -147,22 +147,26 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     const int tot = nunp + L, mns = (int)pm.mns;  // 32-bit: rows per relQuery < 2^31
     nj = tot > 0 && own ? (tot + mns - 1) / mns : 0;
   }
-  int jincl = warp_incl_scan(nj);
+  // draw and PEM-segment offsets in one warp scan: (dcnt << 16) | nj (per-warp
+  // totals stay below 2^16: dcnt <= 2*16-1 and nj <= kMaxJobs per kept relQuery)
+  int incl = warp_incl_scan((dcnt << 16) | nj);
   {  // keep the prefix of relQueries whose segments fit the job buffers
-    const int fit = __popc(__ballot_sync(kFull, lane < n_est && jincl <= kMaxJobs));
+    const int fit = __popc(__ballot_sync(kFull, lane < n_est && (incl & 0xFFFF) <= kMaxJobs));
     if (fit < n_est) {
       n_est = fit;
       if (lane >= n_est) dcnt = nj = nunp = 0;
-      jincl = warp_incl_scan(nj);
+      incl = warp_incl_scan((dcnt << 16) | nj);
     }
   }
   if (n_est == 0) return 0;
-  const int dincl = warp_incl_scan(dcnt);
+  const int jincl = incl & 0xFFFF, dincl = incl >> 16;
   const int doff = dincl - dcnt, jo = jincl - nj;
-  const int D = __shfl_sync(kFull, dincl, 31), J = __shfl_sync(kFull, jincl, 31);
-  {
-    const int nb_items = warp_sum(own ? nunp : 0), nb_samp = warp_sum(own ? (nunp > Ssz ? Ssz : nunp) : 0);
-    if (tid == 0) c.alg_bytes += 4LL * ((long long)nb_items + nb_samp);  // PEM items' tok + sampled tok
+  const int tot_incl = __shfl_sync(kFull, incl, 31);
+  const int D = tot_incl >> 16, J = tot_incl & 0xFFFF;
+  if (warp == 0) {  // PEM items' tok + sampled tok
+    const unsigned nb = own ? (unsigned)(nunp + (nunp > Ssz ? Ssz : nunp)) : 0u;
+    const unsigned tot_b = __reduce_add_sync(kFull, nb);
+    if (lane == 0) c.alg_bytes += 4LL * tot_b;
   }
   phase_mark(c, 5);
   if (warp == 0) {
@@ -310,9 +314,9 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
             rs += r;
             mx = r > mx ? r : mx;
           }
-        ps.n = Le;
-        ps.rsum = warp_sum(rs);
-        ps.rmax = (int)warp_max(mx);
+        ps.n = Le;  // sums of at most mns rows of remaining <= output_limit: 32-bit hardware reductions
+        ps.rsum = __reduce_add_sync(kFull, (unsigned)rs);
+        ps.rmax = (int)__reduce_max_sync(kFull, (unsigned)mx);
       }
       if (lane == 0) S.est_ps[e] = ps;
     }
