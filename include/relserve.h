@@ -60,7 +60,7 @@ typedef struct {
   int64_t max_num_batched_tokens; /* mnbt */
   int64_t sample_size;            /* DPU cache-miss sample size */
   double tau;                     /* starvation threshold (INFINITY disables) */
-  double noise_sigma;             /* world-model noise; only 0 is supported */
+  double noise_sigma;             /* world-model noise (see rs_engine_set_noise) */
   int64_t block_size;             /* prefix-cache block (tokens) */
   int64_t capacity_blocks;        /* prefix-cache capacity (blocks) */
   int64_t iteration_limit;
@@ -139,6 +139,7 @@ typedef struct {
   /* bytes of request / FIFO / log state the iterations had to read or write in
      HBM (the relQuery table and running list live in shared memory) */
   int64_t alg_bytes;
+  int64_t batches;             /* executed prefill/decode batches (= world-model noise draws consumed) */
 } rs_trace_status;
 
 typedef struct rs_engine rs_engine;
@@ -169,6 +170,18 @@ int rs_engine_create(const rs_trace_view* traces, int32_t n_traces, const rs_con
  * on `stream` (a cudaStream_t, NULL = legacy default); does not synchronize.
  */
 int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream);
+
+/*
+ * World-model noise (EngineConfig.noise_sigma > 0, engine.py:310-313): the
+ * reference multiplies each executed batch's duration by 1 + sigma * z, z the
+ * next standard normal of numpy default_rng(SeedSequence([seed, 0xE7])).  That
+ * stream is independent of every scheduling decision, so the caller supplies
+ * its first n values (z[k] for the k-th batch) for trace t (-1: every trace);
+ * a launch that runs out stops early with RS_RUNNING and status.batches == n,
+ * and the caller passes a longer prefix.  Required before stepping when
+ * noise_sigma > 0.
+ */
+int rs_engine_set_noise(rs_engine* e, int32_t t, const double* z, int64_t n);
 
 /* Synchronize `stream` and copy every trace's status to status[n_traces]. */
 int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* status);

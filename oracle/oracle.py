@@ -66,6 +66,8 @@ def lib():
         L.or_run.argtypes = [C.POINTER(_abi.TraceView), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                              C.POINTER(_abi.Config), C.POINTER(_abi.CostModel), C.POINTER(_abi.CostModel),
                              C.POINTER(_abi.Pcg64State), C.c_int32]
+        L.or_run_noise.restype = C.POINTER(_Result)
+        L.or_run_noise.argtypes = L.or_run.argtypes + [C.c_void_p, C.c_int64]
         L.or_free.argtypes = [C.POINTER(_Result)]
         L.or_pem.restype = C.c_int
         L.or_pem.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
@@ -138,8 +140,12 @@ def run(trace, policy: str, world_model, config: EngineConfig | None = None, pol
     if trie is not None:
         args = (_abi.ptr(trie.path_off), _abi.ptr(trie.path_node), _abi.ptr(trie.node_parent),
                 int(trie.node_parent.shape[0]))
-    rp = L.or_run(C.byref(m.view), *args, C.byref(c_cfg), C.byref(world), C.byref(pol), C.byref(rng),
-                  record)
+    noise = np.zeros(0)
+    if cfg.noise_sigma > 0:  # the reference's draws (engine.py:198): one per executed batch, at most one per iteration
+        n = min(int(cfg.iteration_limit), 1 << 22)
+        noise = np.random.default_rng(np.random.SeedSequence([seed, 0xE7])).standard_normal(n)
+    rp = L.or_run_noise(C.byref(m.view), *args, C.byref(c_cfg), C.byref(world), C.byref(pol), C.byref(rng),
+                        record, noise.ctypes.data if len(noise) else None, len(noise))
     try:
         r = rp.contents
         R, N, nl = r.num_relqueries, r.num_requests, r.n_log

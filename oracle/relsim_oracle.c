@@ -502,6 +502,30 @@ or_result* or_run(const rs_trace_view* tr, const int64_t* path_off_in, const int
                   const int32_t* node_parent_in, int64_t n_nodes_in, const rs_config* cfg,
                   const rs_cost_model* world, const rs_cost_model* policy,
                   const rs_pcg64_state* rng, int32_t rec_flags) {
+  return or_run_noise(tr, path_off_in, path_node_in, node_parent_in, n_nodes_in, cfg, world, policy, rng,
+                      rec_flags, NULL, 0);
+}
+
+/* _world_duration (engine.py:310-313): base * (1 + sigma * z) clamped at 0.0,
+   z = the k-th standard normal of the engine's SeedSequence([seed, 0xE7])
+   stream for the k-th executed batch (numpy's draws, passed in). */
+static double world_duration(const rs_config* cfg, const double* noise, int64_t noise_len, int64_t* k,
+                             double base, int* ok) {
+  if (cfg->noise_sigma > 0) {
+    if (*k >= noise_len) {
+      *ok = 0;
+      return base;
+    }
+    const double v = base * (1.0 + cfg->noise_sigma * noise[(*k)++]);
+    base = v > 0.0 ? v : 0.0; /* max(0.0, v) */
+  }
+  return base;
+}
+
+or_result* or_run_noise(const rs_trace_view* tr, const int64_t* path_off_in, const int32_t* path_node_in,
+                        const int32_t* node_parent_in, int64_t n_nodes_in, const rs_config* cfg,
+                        const rs_cost_model* world, const rs_cost_model* policy,
+                        const rs_pcg64_state* rng, int32_t rec_flags, const double* noise, int64_t noise_len) {
   or_result* res = (or_result*)calloc(1, sizeof(or_result));
   if (!res) return NULL;
   const int64_t R = tr->num_relqueries, N = tr->num_requests;
@@ -540,10 +564,12 @@ or_result* or_run(const rs_trace_view* tr, const int64_t* path_off_in, const int
     set_err(res, RS_EINVAL, "tau must be positive");
     return res;
   }
-  if (cfg->noise_sigma > 0) {
-    set_err(res, RS_EUNSUPPORTED, "world-model noise is not restated");
+  if (!(cfg->noise_sigma >= 0)) {
+    set_err(res, RS_EINVAL, "noise_sigma must be non-negative");
     return res;
   }
+  int64_t noise_k = 0;
+  int noise_ok = 1;
   if (use_dpu && cfg->sample_size < 1) {
     set_err(res, RS_EINVAL, "sample_size must be positive");
     return res;
@@ -932,7 +958,12 @@ or_result* or_run(const rs_trace_view* tr, const int64_t* path_off_in, const int
           goto done_loop;
         }
       }
-      double duration = world->alpha_p * (double)ut + world->beta_p;
+      double duration = world_duration(cfg, noise, noise_len, &noise_k, world->alpha_p * (double)ut + world->beta_p,
+                                       &noise_ok);
+      if (!noise_ok) {
+        set_err(res, RS_EINVAL, "noise sequence shorter than the executed batches");
+        goto done_loop;
+      }
       for (int64_t i = 0; i < taken; ++i) {
         int64_t r = pfirst + i;
         e->prefilled[r] = 1;
@@ -951,7 +982,12 @@ or_result* or_run(const rs_trace_view* tr, const int64_t* path_off_in, const int
       rec->batch_first = (int32_t)head_pend;
       rec->batch_n = (int32_t)taken;
     } else if (action == RS_ACTION_DECODE) { /* _execute_decode (engine.py:343-363) */
-      double duration = world->alpha_d * (double)nd + world->beta_d;
+      double duration = world_duration(cfg, noise, noise_len, &noise_k, world->alpha_d * (double)nd + world->beta_d,
+                                       &noise_ok);
+      if (!noise_ok) {
+        set_err(res, RS_EINVAL, "noise sequence shorter than the executed batches");
+        goto done_loop;
+      }
       e->clock += duration;
       int64_t nfin = 0, ndone = 0;
       for (int64_t i = 0; i < nd; ++i) {

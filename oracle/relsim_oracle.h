@@ -79,6 +79,15 @@ or_result* or_run(const rs_trace_view* tr, const int64_t* path_off, const int32_
                   const rs_cost_model* world, const rs_cost_model* policy,
                   const rs_pcg64_state* rng, int32_t record_flags);
 
+/* or_run with world-model noise: noise[k] is the standard normal the reference
+   draws for its k-th executed batch (engine.py:310-313); needed when
+   cfg->noise_sigma > 0. */
+or_result* or_run_noise(const rs_trace_view* tr, const int64_t* path_off, const int32_t* path_node,
+                        const int32_t* node_parent, int64_t n_nodes, const rs_config* cfg,
+                        const rs_cost_model* world, const rs_cost_model* policy,
+                        const rs_pcg64_state* rng, int32_t record_flags, const double* noise,
+                        int64_t noise_len);
+
 void or_free(or_result* r);
 
 /* pem() over explicit items (priority.py:163-218). Returns RS_EINFEASIBLE on utok > cap. */

@@ -89,6 +89,7 @@ class TraceStatus(C.Structure):
         ("cache_miss_tokens", C.c_int64), ("kv_reserved", C.c_int64), ("n_log", C.c_int64),
         ("live_relqueries", C.c_int64), ("admitted", C.c_int64), ("status", C.c_int32),
         ("error_detail", C.c_int32), ("rng", Pcg64State), ("phase_cycles", C.c_int64 * 23), ("alg_bytes", C.c_int64),
+        ("batches", C.c_int64),
     ]
 
 

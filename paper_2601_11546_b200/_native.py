@@ -74,6 +74,8 @@ def lib():
     L.rs_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p]
     L.rs_ipc_open_handle.restype = C.c_int
     L.rs_ipc_open_handle.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.rs_engine_set_noise.restype = C.c_int
+    L.rs_engine_set_noise.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]
     L.rs_ipc_close.restype = C.c_int
     L.rs_ipc_close.argtypes = [C.c_void_p]
     _lib = L
@@ -86,7 +88,7 @@ EXPORTED_SYMBOLS = (
     "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_destroy",
     "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
-    "rs_ipc_open_handle", "rs_ipc_close",
+    "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise",
 )
 
 
@@ -166,6 +168,11 @@ class NativeEngine:
             self._opened.append(p.value)
             ptrs[d] = p
         _check(lib().rs_engine_connect(self.h, ptrs))
+
+    def set_noise(self, t: int, z: np.ndarray):
+        """World-model noise draws for trace t (-1: all), include/relserve.h rs_engine_set_noise."""
+        z = np.ascontiguousarray(z, np.float64)
+        _check(lib().rs_engine_set_noise(self.h, t, z.ctypes.data if len(z) else None, len(z)))
 
     def step(self, max_iters: int, stream=None):
         _check(lib().rs_engine_step(self.h, int(max_iters), _stream_ptr(stream)))

@@ -44,6 +44,16 @@ namespace rsd {
 // One scheduler iteration (all threads).  Returns false when the trace stopped.
 // ---------------------------------------------------------------------------
 
+// _world_duration (engine.py:310-313): base * (1 + sigma * z), clamped at 0,
+// z = the n-th standard normal of the engine's noise stream (one per executed batch)
+__device__ __forceinline__ double world_duration(const Params& P, const TraceDev& T, long long n, double base) {
+  if (P.cfg.noise_sigma > 0) {
+    const double v = __dmul_rn(base, __dadd_rn(1.0, __dmul_rn(P.cfg.noise_sigma, T.noise[n])));
+    base = v > 0.0 ? v : 0.0;  // max(0.0, v)
+  }
+  return base;
+}
+
 template <bool kFast>
 __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   Ctl& c = S.c;
@@ -60,6 +70,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     } else if (c.iteration >= cfg.iteration_limit) {
       c.status = RS_EABORT_LIMIT;
       S.go = 0;
+    } else if (cfg.noise_sigma > 0 && c.n_batch >= T.noise_n) {
+      S.go = 0;  // out of noise draws: end the launch, still running (the host appends more)
     } else {
       int a = c.n_admitted;
       const int a0 = a;
@@ -398,7 +410,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       if (ok) {
         c.alg_bytes += 16LL * n;  // FIFO pushes (window reads are counted in prefill_fast)
         const double start = c.clock;
-        const double dur = __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p);
+        const double dur =
+            world_duration(P, T, c.n_batch++, __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p));
         c.n_run = n_run0 + n;
         rq.q[h] = q + n;
         if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
@@ -450,7 +463,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       S.rrq_dirty = 0;
     }
     __syncthreads();
-    const double clk = __dadd_rn(c.clock, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d));
+    const double clk = __dadd_rn(
+        c.clock, world_duration(P, T, c.n_batch, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d)));
     int kv_free = 0;
     int keep[kMaxRun / kThreads], nrow[kMaxRun / kThreads], nrank[kMaxRun / kThreads];
     int ngen[kMaxRun / kThreads], nout[kMaxRun / kThreads], nkv[kMaxRun / kThreads];
@@ -510,6 +524,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       c.n_run = cbase;
       c.kv -= kv_total;
       c.clock = clk;
+      c.n_batch++;
       if (cfg.log_decisions && T.log_cap > 0) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
       if (S.rrq_dirty) {
         int w = 0;
@@ -748,6 +763,7 @@ struct HostTrace {
   // one device arena per trace (a cudaMalloc per buffer costs more than the upload itself)
   char* arena = nullptr;
   size_t arena_cap = 0, arena_used = 0;
+  double* noise_buf = nullptr;  // rs_engine_set_noise
 };
 
 // Reserve the trace's arena: every dalloc below carves from it (256-byte aligned).
@@ -822,7 +838,7 @@ static int validate_config(const rs_config* cfg) {
     return fail(RS_EINVAL, "block_size and capacity_blocks must be positive");
   const bool dpu = cfg->policy >= RS_POLICY_RELSERVE;
   if (dpu && !(cfg->tau > 0)) return fail(RS_EINVAL, "tau must be positive");
-  if (cfg->noise_sigma > 0) return fail(RS_EUNSUPPORTED, "world-model noise is not on the device path");
+  if (!(cfg->noise_sigma >= 0)) return fail(RS_EINVAL, "noise_sigma must be non-negative");
   if (dpu && cfg->sample_size < 1) return fail(RS_EINVAL, "sample_size must be positive");
   if (dpu && cfg->sample_size > kMaxSample)
     return fail(RS_EUNSUPPORTED, "sample_size above the device limit (64)");
@@ -1215,8 +1231,29 @@ int rs_ipc_close(void* dptr) {
   return RS_OK;
 }
 
+int rs_engine_set_noise(rs_engine* e, int32_t t, const double* z, int64_t n) {
+  if (!e || t < -1 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
+  if (n < 0 || (n > 0 && !z)) return fail(RS_EINVAL, "bad noise buffer");
+  RS_CUDA(cudaSetDevice(e->device));
+  for (int i = 0; i < (int)e->traces.size(); ++i) {
+    if (t >= 0 && i != t) continue;
+    HostTrace& h = e->traces[i];
+    double* d = nullptr;
+    RS_CUDA(cudaMalloc(&d, std::max<int64_t>(n, 1) * sizeof(double)));
+    if (n) RS_CUDA(cudaMemcpy(d, z, n * sizeof(double), cudaMemcpyHostToDevice));
+    if (h.noise_buf) cudaFree(h.noise_buf);
+    h.noise_buf = d;
+    h.dev.noise = d;
+    h.dev.noise_n = n;
+  }
+  return upload_traces(e);
+}
+
 int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
   if (!e) return fail(RS_EINVAL, "null engine");
+  if (e->params.cfg.noise_sigma > 0)
+    for (auto& h : e->traces)
+      if (!h.noise_buf) return fail(RS_EINVAL, "noise_sigma > 0 needs rs_engine_set_noise before stepping");
   if (e->shard_world > 1 && !e->connected) return fail(RS_EINVAL, "sharded engine not connected to its peers");
   RS_CUDA(cudaSetDevice(e->device));
   long long cap = e->params.cfg.log_decisions ? e->traces[0].dev.log_cap : max_iters;
@@ -1254,6 +1291,7 @@ int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* st) {
     s.rng = c->rng;
     for (int k = 0; k < 23; ++k) s.phase_cycles[k] = c->phase[k];
     s.alg_bytes = c->alg_bytes;
+    s.batches = c->n_batch;
   }
   return RS_OK;
 }
@@ -1339,8 +1377,10 @@ void rs_engine_destroy(rs_engine* e) {
   cudaSetDevice(e->device);
   if (e->mbox) cudaFree(e->mbox);
   if (e->d_peers) cudaFree(e->d_peers);
-  for (auto& h : e->traces)
+  for (auto& h : e->traces) {
     for (void* p : h.allocs) cudaFree(p);
+    if (h.noise_buf) cudaFree(h.noise_buf);
+  }
   if (e->d_traces) cudaFree(e->d_traces);
   delete e;
 }

@@ -60,6 +60,7 @@ struct alignas(16) Ctl {
   long long count;            // resident blocks
   long long n_log;
   long long alg_bytes;  // HBM/L2 bytes the algorithm must move
+  long long n_batch;    // executed batches = world-model noise draws consumed (engine.py:310-313)
   long long fifo_head, fifo_tail;
   int n_admitted, live;
   int n_run, n_act;
@@ -149,6 +150,8 @@ struct TraceDev {
   int pad1;
   ShardRec* self_mbox;       // this shard's mailbox ShardRec[world][2] (shard.cuh)
   ShardRec* const* peers;    // [world] every shard's mailbox, as addressable from this device
+  const double* noise;       // world-model noise: standard normals of the SeedSequence([seed, 0xE7]) stream
+  long long noise_n;         // ... available (rs_engine_set_noise)
   rs_iter_record* log;
   long long log_cap;
   Ctl* ctl;

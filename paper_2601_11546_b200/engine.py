@@ -214,6 +214,8 @@ class Engine:
 
     #: iterations launched per device step (one persistent-kernel launch)
     chunk_iterations = 1 << 14
+    #: world-model noise draws handed to the device first (the prefix doubles when used up)
+    noise_chunk = 1 << 14
 
     def __init__(
         self,
@@ -245,9 +247,8 @@ class Engine:
         c = self.config
         if policy in ("relserve", "relserve-pp", "relserve-dp") and not (c.tau > 0):
             raise ValueError("tau must be positive")
-        if c.noise_sigma > 0:
-            raise NotImplementedError(
-                "world-model noise (numpy standard_normal replay) is not on the device path yet")
+        if c.noise_sigma < 0:
+            raise ValueError("noise_sigma must be non-negative")
         from . import _native
 
         self._m = _marshal.marshal_trace(trace, c.block_size, policy, self.policy_model,
@@ -258,6 +259,13 @@ class Engine:
             log_capacity=self.chunk_iterations if c.log_decisions else 0, shards=shards, rank=shard_rank,
         )
         self.shards, self.shard_rank = shards, shard_rank
+        # world-model noise (engine.py:198, 310-313): the reference's standard normals, one per
+        # executed batch, from the same stream; handed to the device in growing prefixes
+        self._noise_rng = None
+        self._noise = np.zeros(0)
+        if c.noise_sigma > 0:
+            self._noise_rng = np.random.default_rng(np.random.SeedSequence([seed, 0xE7]))
+            self._extend_noise(self.noise_chunk)
         self.iteration = 0
         self.clock = 0.0
         self.kv_reserved = 0
@@ -277,11 +285,25 @@ class Engine:
 
     # -- device loop ---------------------------------------------------------
 
+    def _extend_noise(self, n: int) -> None:
+        self._noise = np.concatenate([self._noise, self._noise_rng.standard_normal(n)])
+        self._native.set_noise(-1, self._noise)
+
     def step(self, max_iterations: int) -> _abi.TraceStatus:
         """Run up to max_iterations scheduler iterations on the device."""
         ne = self._native
-        ne.step(max_iterations, self.stream)
-        st = ne.status(self.stream)[0]
+        done = 0
+        while True:
+            it0 = self.iteration
+            ne.step(max_iterations - done, self.stream)
+            st = ne.status(self.stream)[0]
+            self.iteration = st.iterations
+            done += st.iterations - it0
+            # a launch that ran out of noise draws stops early, still running
+            if (self._noise_rng is None or st.status != _abi.RS_RUNNING or st.batches < len(self._noise)
+                    or done >= max_iterations):
+                break
+            self._extend_noise(len(self._noise))
         if self.config.log_decisions and st.n_log > self._n_read:
             self._records.append(ne.read_log(0, self._n_read, st.n_log - self._n_read))
             self._n_read = st.n_log

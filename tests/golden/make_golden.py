@@ -298,6 +298,11 @@ CASES = {
                         policy="relserve", world="llama-70b-like", full=False),
     "cfg4_cell_b": dict(spec=gen({"num_relqueries": 100, "size_range": [1, 64], "rate": 0.25, "seed": 300}),
                         policy="relserve", world="opt-13b-like", full=False),
+    # world-model noise (engine.py:310-313): noisy batch durations
+    "noise_relserve": dict(spec=gen({"num_relqueries": 40, "size_range": [1, 60], "rate": 2.0, "seed": 13}),
+                           policy="relserve", world="opt-13b-like", config={"noise_sigma": 0.1}, seed=4),
+    "noise_fcfs": dict(spec=gen({"num_relqueries": 30, "size_range": [1, 40], "rate": 3.0, "seed": 14}),
+                       policy="fcfs", world=list(TEST_MODEL), config={"noise_sigma": 0.5}, seed=2),
     # configs 2 / 3: windowed (first 40 iterations)
     "cfg2_window": dict(spec=gen({"num_relqueries": 1000, "size_range": [1000, 1000], "rate": 1e6, "seed": 0}),
                         policy="relserve", world="opt-13b-like", window=40, full=False),

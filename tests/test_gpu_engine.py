@@ -90,3 +90,19 @@ def test_device_matches_oracle_random_traces(case, oracle_mod):
     assert np.array_equal(res.completion_iteration, ref.completion_iter)
     assert res.sim_duration == ref.clock
     assert (res.cache_hit_tokens, res.cache_miss_tokens) == (ref.cache_hit_tokens, ref.cache_miss_tokens)
+
+
+@pytest.mark.parametrize("chunk", [3, 64])
+def test_noise_prefix_refill_matches_reference_golden(chunk, monkeypatch):
+    """World-model noise handed to the device in short prefixes (launches stop when
+    they run out, the host doubles the prefix) gives the reference's run."""
+    from paper_2601_11546_b200.engine import Engine
+
+    monkeypatch.setattr(Engine, "noise_chunk", chunk)
+    g = load_golden("noise_relserve")
+    trace, policy, world, cfg, pm, seed = parity.golden_inputs(g)
+    res, aborted = run_device(trace, policy, world, cfg, pm, seed)
+    assert aborted is None
+    parity.compare_records(res.records, g, trace, f"noise/{chunk}")
+    parity.compare_completion(res.completion_iteration, g, trace)
+    assert res.sim_duration == g["result"]["sim_duration"]

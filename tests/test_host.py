@@ -83,8 +83,8 @@ def test_api_validation_before_any_device_work():
         Engine(t, "srpt", w)
     with pytest.raises(ValueError):
         Engine(t, "relserve", w, EngineConfig(tau=0.0))
-    with pytest.raises(NotImplementedError):
-        Engine(t, "relserve", w, EngineConfig(noise_sigma=0.1))
+    with pytest.raises(ValueError):
+        Engine(t, "relserve", w, EngineConfig(noise_sigma=-0.1))
 
 
 def test_no_cpu_fallback_without_a_gpu():
