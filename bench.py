@@ -434,52 +434,109 @@ def run_config4(args, ws, rank, local):
         model, rate, s = cells[ci]
         t = generate_trace(TraceConfig(num_relqueries=100, size_range=(1, s), rate=rate, seed=ci))
         groups.setdefault(model, []).append((ci, t))
-    engines = []
-    for model, items in groups.items():
-        w = world_preset(model)
-        ms = [_marshal.marshal_trace(t, cfg.block_size, "relserve", w) for _, t in items]
-        ne = NativeEngine([m.view for m in ms], _marshal.make_config(cfg, "relserve"), _marshal.make_model(w),
-                          _marshal.make_model(w), [_marshal.dpu_rng_state(ci) for ci, _ in items], local,
-                          log_capacity=0)
-        engines.append((ne, ms, torch.cuda.Stream(dev)))
+    models = list(groups.items())
+
+    def make_engines():
+        out = []
+        for model, items in models:
+            w = world_preset(model)
+            ms = [_marshal.marshal_trace(t, cfg.block_size, "relserve", w) for _, t in items]
+            ne = NativeEngine([m.view for m in ms], _marshal.make_config(cfg, "relserve"), _marshal.make_model(w),
+                              _marshal.make_model(w), [_marshal.dpu_rng_state(ci) for ci, _ in items], local,
+                              log_capacity=0)
+            out.append((ne, ms))
+        return out
+
+    streams = [torch.cuda.Stream(dev) for _ in models]
+    main_s = torch.cuda.current_stream(dev)
+
+    def sweep(timed):
+        """One step: every trace of this GPU's share run to completion (one launch per cost model,
+        the launches concurrent on their own streams); engines are rebuilt outside the events."""
+        engines = make_engines()
+        torch.cuda.synchronize(dev)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(main_s)
+        for (ne, _), st in zip(engines, streams):
+            st.wait_event(a)
+            ne.step(1 << 30, st)  # one launch runs every trace to completion
+            e = torch.cuda.Event()
+            e.record(st)
+            main_s.wait_event(e)
+        b.record(main_s)
+        torch.cuda.synchronize(dev)
+        iters = 0
+        for ne, _ in engines:
+            for st in ne.status():
+                assert st.status == _abi.RS_OK, st.status
+                iters += st.iterations
+            ne.close()
+        return a.elapsed_time(b) / 1e3, iters
+
+    for _ in range(args.warmup):
+        sweep(False)
     if ws > 1:
         import torch.distributed as dist
 
         dist.barrier()
-    torch.cuda.synchronize(dev)
+    dev_s, iters = 0.0, 0
     t0 = time.perf_counter()
-    evs = []
     with ClockSampler(local) as clk:
-        for ne, _, st in engines:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(st)
-            ne.step(1 << 30, st)  # one launch runs every trace to completion
-            b.record(st)
-            evs.append((a, b))
-        torch.cuda.synchronize(dev)
+        for _ in range(args.steps):
+            d, n = sweep(True)
+            dev_s += d
+            iters += n
     wall = time.perf_counter() - t0
-    dev_s = max(a.elapsed_time(b) for a, b in evs) / 1e3
-    iters = 0
-    for ne, _, _ in engines:
-        for st in ne.status():
-            assert st.status == _abi.RS_OK, st.status
-            iters += st.iterations
-        ne.close()
     t_max = max_over_ranks(dev_s, ws, dev)
     total = sum_over_ranks(float(iters), ws, dev)
     if rank != 0:
         return None
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        cpu = cpu_baseline_config4([cells[ci] + (ci,) for ci in mine])
     return {
         "metric": "sched iters/sec, config-4 sweep (aggregate over independent traces)",
-        "value": total / t_max, "unit": "iters/s", "n_gpus": ws, "steps": 1, "warmup": 0,
-        "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "value": total / t_max, "unit": "iters/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64+int32", "data": "synthetic (generate_trace per config-4 cell)",
         "config": {"workload": f"config4: {args.traces_per_gpu} traces/GPU of 100 relQ, sizes (1,s) s=8..1000, "
-                               "rates 0.25..4, opt-13b/llama-70b, full runs", "traces_per_gpu": len(mine)},
-        "iterations_timed": int(total), "gpu_launches": len(engines), "clocks": clk.summary(),
-        "host_wall_s": wall,
+                               "rates 0.25..4, opt-13b/llama-70b, full runs; a step = every trace of the share "
+                               "run to completion", "traces_per_gpu": len(mine),
+                   "l2": "working set of each step is fresh (engines rebuilt between steps)"},
+        "iterations_timed": int(total), "gpu_launches": len(models) * args.steps, "clocks": clk.summary(),
+        "host_wall_s": wall, "cpu_baseline": cpu,
     }
+
+
+def _cpu_cell(cell):
+    """One config-4 cell on the oracle (child process of cpu_baseline_config4)."""
+    import time as _t
+
+    from oracle import oracle
+    from paper_2601_11546_b200 import EngineConfig, TraceConfig, generate_trace, world_preset
+
+    model, rate, s, ci = cell
+    t = generate_trace(TraceConfig(num_relqueries=100, size_range=(1, s), rate=rate, seed=ci))
+    t0 = _t.perf_counter()
+    r = oracle.run(t, "relserve", world_preset(model), EngineConfig(), None, ci)
+    return r.iterations, _t.perf_counter() - t0
+
+
+def cpu_baseline_config4(cells):
+    """the oracle over the same cells, full runs, a process pool over all host cores
+    (the reference's `relsim run --jobs` pattern, cli.py:194-196)."""
+    import multiprocessing as mp
+
+    n = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(n) as pool:
+        res = pool.map(_cpu_cell, cells, chunksize=1)
+    wall = time.perf_counter() - t0
+    iters = sum(r[0] for r in res)
+    return {"value": iters / wall, "unit": "iters/s", "cores": n, "kind": "port",
+            "sample": f"the same {len(cells)} cells, full runs, {n}-process pool; {iters} iterations in {wall:.1f} s "
+                      "(incl. pool start-up)", "cpu": _cpu_model()}
 
 
 def main():
