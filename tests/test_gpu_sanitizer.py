@@ -26,6 +26,15 @@ for policy, tc, kw in [("sp", dict(num_relqueries=40, size_range=(1, 40), rate=1
     except SimulationAborted:
         pass
     e.close()
+# sharded pool (3 shards as CTAs of one launch) with world-model noise
+t = generate_trace(TraceConfig(num_relqueries=60, size_range=(1, 50), rate=6.0, seed=8))
+e = Engine(t, "relserve", world_preset("llama-70b-like"), EngineConfig(iteration_limit=80, noise_sigma=0.2),
+           shards=3)
+try:
+    e.run()
+except SimulationAborted:
+    pass
+e.close()
 print("ran")
 """
 
@@ -37,7 +46,7 @@ def _sanitizer():
     return None
 
 
-@pytest.mark.parametrize("tool", ["racecheck", "memcheck"])
+@pytest.mark.parametrize("tool", ["racecheck", "memcheck", "synccheck"])
 def test_sanitizer_clean(tool, tmp_path):
     cs = _sanitizer()
     if cs is None:
