@@ -19,6 +19,15 @@ __device__ __forceinline__ int opaque_warp() {
   return (int)(t >> 5);
 }
 
+// Lane index with the same property: conditions on it cannot be related to
+// threadIdx.x (or to each other) at compile time, so lane-0-only blocks end at
+// a reconvergence point before the next warp-wide shuffle / ballot.
+__device__ __forceinline__ int opaque_lane() {
+  unsigned l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return (int)l;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
   const int lane = threadIdx.x & 31;

@@ -329,7 +329,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
 #define RS_JOB_META(j)                                                               \
   int e = 0;                                                                         \
   for (int x = 0; x < n_est; ++x)                                                    \
-    if (__shfl_sync(kFull, jo, x) <= (j) && __shfl_sync(kFull, nj, x) > 0) e = x;    \
+    if ((__shfl_sync(kFull, jo, x) <= (j)) & (__shfl_sync(kFull, nj, x) > 0)) e = x;  \
   const int k = (j) - __shfl_sync(kFull, jo, e);                                     \
   const int ne = __shfl_sync(kFull, nunp, e);                                        \
   const int Le = __shfl_sync(kFull, L, e);                                           \
