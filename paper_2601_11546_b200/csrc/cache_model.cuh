@@ -212,10 +212,10 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   const int m0 = rq.m[h];
   const unsigned long long tc = c.tclock;
   const long long head0 = c.fifo_head, tail0 = c.fifo_tail, count0 = c.count;
-  if (tid == 0) S.fp_bad = 0;
-  __syncthreads();
+  // 1. per-row tail blocks: prefix sums of (tail, tok, tail-less rows) in one scan
   long long Tv[kMaxRun / kThreads], inclT[kMaxRun / kThreads];
   long long cT = 0, cTok = 0;
+  int n_bad = 0;
 #pragma unroll
   for (int s = 0; s < kMaxRun / kThreads; ++s) {
     Tv[s] = 0;
@@ -226,23 +226,23 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
       if (i < n) {
         tk = tokv[i];
         tl = (int)(tk / B) - Pc;
-        if (tl <= 0) S.fp_bad = 1;
       }
-      int v[2] = {tl, tk}, tot[2];
-      block_scan32<2>(v, S.s32, tot);
+      int v[3] = {tl, tk, (i < n && tl <= 0) ? 1 : 0}, tot[3];
+      block_scan32<3>(v, S.s32, tot);
       Tv[s] = tl;
       inclT[s] = cT + v[0];
       cT += tot[0];
       cTok += tot[1];
+      n_bad += tot[2];
     }
   }
   const long long newn = (long long)(Pc - m0) + cT;
   const long long E = count0 + newn > C ? count0 + newn - C : 0;
   const long long n_old = tail0 - head0;
   const int Wn = (int)(E < n_old ? E : n_old);
-  if (S.fp_bad || E > count0 - m0 || Wn > kWin) return false;
+  if (n_bad || E > count0 - m0 || Wn > kWin) return false;  // block-uniform
   phase_mark(c, 13);
-  // FIFO pushes: row i's chain / tail touch times from prefix sums of touches
+  // 2. FIFO pushes: row i's chain / tail touch times from prefix sums of touches
 #pragma unroll
   for (int s = 0; s < kMaxRun / kThreads; ++s) {
     const int i = s * kThreads + tid;
@@ -259,7 +259,8 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
       if (i == n - 1) S.fp_c0_last = c0i;
     }
   }
-  // stage the FIFO head (the oldest tails) and their relQueries' chain state
+  //    stage the FIFO head (the oldest tails) and their relQueries' chain state;
+  //    thread 0 meanwhile drops h from the chain candidates (its chain is touched)
   for (int j = tid; j < Wn; j += kThreads) {
     const FifoEnt e = T.fifo[(head0 + j) & (T.fifo_cap - 1)];
     S.win.t0[j] = e.t0;
@@ -270,33 +271,32 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
     atomicAdd(&rq.scr_cnt[e.rank], 1);
     atomicMax(&rq.scr_last[e.rank], j);
   }
-  __syncthreads();
-  for (int j = tid; j < Wn; j += kThreads) {
-    const int a = S.win.rank[j];
-    S.win.last[j] = (a != h && rq.scr_last[a] == j && rq.scr_cnt[a] == rq.ntails[a]) ? 1 : 0;
-  }
-  __syncthreads();
-  phase_mark(c, 14);
   if (tid == 0) {
     c.alg_bytes += 16LL * Wn;  // staged FIFO head
     cc_remove(c, h);
     S.fp_par = c.cc_n == 0;
     S.fp_cut = 0x7FFFFFFF;
-    S.fp_bad = 0;
   }
   __syncthreads();
-  // Parallel drain (no chain candidate pending): in LRU order the FIFO units
+  phase_mark(c, 14);
+  // 3. Parallel drain (no chain candidate pending): in LRU order the FIFO units
   // are consumed front to back, each relQuery's chain right after its last
   // tail -- provided that chain is older than the next unit's leaf.  Blocks
-  // per unit b_j = tres_j (+ m_j if last); the cut is the first unit whose
-  // inclusive sum reaches E.
+  // per unit b_j = tres_j (+ m_j if it is the relQuery's last resident tail);
+  // the cut is the first unit whose inclusive sum reaches E.  The thread of
+  // unit j computes its `last` flag itself, so no barrier separates them.
   bool par = S.fp_par;
   if (par && E > 0) {
     long long carry = 0;
     for (int base = 0; base < Wn; base += kThreads) {
       const int j = base + tid;
       int bj = 0;
-      if (j < Wn) bj = S.win.tres[j] + (S.win.last[j] ? S.win.mm[j] : 0);
+      if (j < Wn) {
+        const int a = S.win.rank[j];
+        const int last = (a != h && rq.scr_last[a] == j && rq.scr_cnt[a] == rq.ntails[a]) ? 1 : 0;
+        S.win.last[j] = last;
+        bj = S.win.tres[j] + (last ? S.win.mm[j] : 0);
+      }
       int v[1] = {bj}, tot[1];
       block_scan32<1>(v, S.s32, tot);
       if (j < Wn && carry + v[0] >= E && carry + v[0] - bj < E) {  // the unique cut unit
@@ -311,17 +311,17 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
       par = false;
     } else {
       const long long rem_cut = S.fp_rem;
+      bool bad = false;
       for (int j = tid; j <= cut && j < Wn; j += kThreads) {
         const bool chain_evicted = S.win.last[j] && (j < cut || rem_cut > S.win.tres[j]);
         if (chain_evicted) {
           const unsigned long long kc = S.win.c0[j] + (unsigned long long)(S.win.mm[j] - 1);
           const bool next_in = j + 1 < Wn;
           const unsigned long long kn = next_in ? S.win.t0[j + 1] + (unsigned long long)(S.win.tres[j + 1] - 1) : ~0ULL;
-          if ((!next_in && j + 1 < n_old) || !(kc < kn)) S.fp_bad = 1;
+          if ((!next_in && j + 1 < n_old) || !(kc < kn)) bad = true;
         }
       }
-      __syncthreads();
-      par = !S.fp_bad;
+      par = !__syncthreads_or(bad);
       if (par) {
         for (int j = tid; j < cut; j += kThreads) {
           atomicSub(&rq.ntails[S.win.rank[j]], 1);
@@ -346,18 +346,27 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
             }
           }
           c.count -= E;
-          S.fp_popped = -1;  // ntails already adjusted
           c.fifo_head = head0 + head_adv;
         }
       }
     }
   } else if (par && tid == 0) {
-    S.fp_popped = -1;
     c.fifo_head = head0;
   }
-  __syncthreads();
+  // 4. sequential drain (cold path) and the batch's own bookkeeping (thread 0);
+  //    h's tail count is updated atomically: drain threads may be retiring h's older tails
+  if (!par) {
+    if (tid == 0) {
+      // the last flags for the sequential drain (the parallel branch computed them itself)
+      for (int j = 0; j < Wn; ++j) {
+        const int a = S.win.rank[j];
+        S.win.last[j] = (a != h && rq.scr_last[a] == j && rq.scr_cnt[a] == rq.ntails[a]) ? 1 : 0;
+      }
+      drain_sequential(S, T, E, Wn, head0);
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
-    if (!par) drain_sequential(S, T, E, Wn, head0);  // cold path, out of line
     const long long hitb = (long long)m0 + (long long)(n - 1) * Pc;
     c.hit += B * hitb;
     c.miss += cTok - B * hitb;
@@ -367,18 +376,17 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
     c.fifo_tail = tail0 + n;
     rq.m[h] = Pc;
     rq.c0[h] = S.fp_c0_last;
-    rq.ntails[h] += n;
+    atomicAdd(&rq.ntails[h], n);
   }
-  __syncthreads();
-  const int popped = S.fp_popped;  // -1: the parallel drain adjusted ntails itself
+  // 5. reset the staging counters; the sequential drain's popped units lose a tail
+  const int popped = par ? 0 : S.fp_popped;
   for (int j = tid; j < Wn; j += kThreads) {
     const int a = S.win.rank[j];
     if (j < popped) atomicSub(&rq.ntails[a], 1);
     rq.scr_cnt[a] = 0;
     rq.scr_last[a] = -1;
   }
-  __syncthreads();
-  return true;
+  return true;  // the caller's next barrier orders these writes
 }
 
 }  // namespace rsd
