@@ -103,3 +103,41 @@ def test_sharded_policies(policy, tau, oracle_mod):
     assert ref.status == 0
     assert b.iterations == ref.iterations and b.sim_duration == ref.clock
     assert np.array_equal(b.completion_iteration, ref.completion_iter)
+
+
+def test_two_process_shards_over_ipc(tmp_path):
+    """Two processes, one shard each, mailboxes mapped with CUDA IPC and handles
+    swapped over a gloo group (sharded.connect): the multi-GPU code path, here with
+    both processes time-sliced on GPU 0.  Bit-identical to the unsharded run."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    from paper_2601_11546_b200 import EngineConfig, TraceConfig, generate_trace, world_preset
+
+    iters = 30
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    worker = Path(__file__).with_name("ipc_shard_worker.py")
+    env = dict(__import__("os").environ, RS_IPC_ITERS=str(iters))
+    procs = [subprocess.Popen([sys.executable, str(worker), str(r), "2", str(port), str(tmp_path / f"r{r}.npy")],
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT) for r in range(2)]
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=240)[0].decode()[-2000:])
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+    assert all(p.returncode == 0 for p in procs), outs
+    trace = generate_trace(TraceConfig(num_relqueries=40, size_range=(1, 60), rate=4.0, seed=9))
+    ref, _ = run(trace, "relserve", world_preset("opt-13b-like"), EngineConfig(iteration_limit=iters), None, 0, 1)
+    for r in range(2):
+        got = np.load(tmp_path / f"r{r}.npy")
+        assert len(got) == len(ref.records) == iters
+        for k in FIELDS:
+            assert np.array_equal(got[k], ref.records[k], equal_nan=got[k].dtype.kind == "f"), (r, k)
