@@ -268,39 +268,7 @@ def run_ours(args, ws, rank, local):
     # ---- end to end through the public API (host buffers, copies inside)
     e2e = None
     if not args.no_e2e:
-        torch.cuda.synchronize(dev)
-        import gc
-
-        gc.collect()
-        t0 = time.perf_counter()
-        eng = Engine(trace, "relserve", world, cfg, seed=0, device=local, stream=stream, shards=shards,
-                     shard_rank=srank)
-        if pool and ws > 1:
-            from paper_2601_11546_b200 import sharded
-
-            sharded.connect(eng)
-        eng.chunk_iterations = I
-        t1 = time.perf_counter()
-        st0 = eng.step(WINDOW_START)
-        for _ in range(args.steps):
-            eng.step(I)
-        t2 = time.perf_counter()
-        res = eng._collect(0.0)
-        torch.cuda.synchronize(dev)
-        wall = time.perf_counter() - t0
-        e2e_parts = {"create_ms": 1e3 * (t1 - t0), "steps_ms": 1e3 * (t2 - t1),
-                     "collect_ms": 1e3 * (time.perf_counter() - t2)}
-        e_iters = eng.iteration
-        eng.close()
-        h2d = sum(v.nbytes for v in m.arrays.values() if v is not None)
-        d2h_step = I * 96 + 128
-        d2h_final = c.num_requests * (4 + 1 + 8 + 8) + c.num_relqueries * 32
-        wall_max = max_over_ranks(wall, ws, dev)
-        e2e_total = float(e_iters) if pool else sum_over_ranks(float(e_iters), ws, dev)
-        e2e = {"value": e2e_total / wall_max, "unit": "iters/s",
-               "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / args.steps),
-               "iterations": int(e_iters), "wall_s": wall_max, "breakdown_ms": e2e_parts,
-               "includes": "trace upload, iterations 0..window end (incl. first-sight DPU), per-step record readback, final ledger/request readback"}
+        e2e = e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, srank)
 
     out = None
     if rank == 0:
@@ -343,6 +311,66 @@ def run_ours(args, ws, rank, local):
             "cpu_baseline": cpu,
         }
     return out
+
+
+#: end-to-end repetitions: the host-side parts (engine creation, result collection) see OS
+#: noise of several ms, so the run is repeated and the median reported (every run listed)
+E2E_REPEATS = 3
+
+
+def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, srank):
+    """The bench window through the public `Engine` API from host arrays: trace upload and
+    first-sight kernel (engine creation), every step's launch + status + decision-record
+    readback, and the final ledger / completion readback, wall-clock timed."""
+    import gc
+
+    import torch
+
+    from paper_2601_11546_b200.engine import Engine
+
+    I = args.iters_per_step
+    c = trace.columns()
+    runs = []
+    for rep in range(E2E_REPEATS + 1):  # run 0: untimed warm-up of the host path (allocator, first-call costs)
+        torch.cuda.synchronize(dev)
+        gc.collect()
+        t0 = time.perf_counter()
+        eng = Engine(trace, "relserve", world, cfg, seed=0, device=local, stream=stream, shards=shards,
+                     shard_rank=srank)
+        if pool and ws > 1:
+            from paper_2601_11546_b200 import sharded
+
+            sharded.connect(eng)
+        eng.chunk_iterations = I
+        t1 = time.perf_counter()
+        eng.step(WINDOW_START)
+        for _ in range(args.steps):
+            eng.step(I)
+        t2 = time.perf_counter()
+        eng._collect(0.0)
+        torch.cuda.synchronize(dev)
+        t3 = time.perf_counter()
+        e_iters = eng.iteration
+        eng.close()
+        wall = max_over_ranks(t3 - t0, ws, dev)
+        total = float(e_iters) if pool else sum_over_ranks(float(e_iters), ws, dev)
+        if rep == 0:
+            continue
+        runs.append({"value": total / wall, "wall_s": wall, "iterations": int(e_iters),
+                     "breakdown_ms": {"create_ms": 1e3 * (t1 - t0), "steps_ms": 1e3 * (t2 - t1),
+                                      "collect_ms": 1e3 * (t3 - t2)}})
+    med = sorted(runs, key=lambda r: r["value"])[len(runs) // 2]
+    h2d = sum(v.nbytes for v in m.arrays.values() if v is not None)
+    d2h_step = I * 96 + 128
+    d2h_final = c.num_requests * 4 + c.num_relqueries * 32
+    return {"value": med["value"], "unit": "iters/s",
+            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / args.steps),
+            "iterations": med["iterations"], "wall_s": med["wall_s"], "breakdown_ms": med["breakdown_ms"],
+            "runs": [{"value": round(r["value"], 1), **{k: round(v, 2) for k, v in r["breakdown_ms"].items()}}
+                     for r in runs],
+            "statistic": f"median of {E2E_REPEATS} runs after one untimed warm-up run",
+            "includes": "trace upload, iterations 0..window end (incl. first-sight DPU), per-step record "
+                        "readback, final ledger/completion readback"}
 
 
 def cpu_baseline(args, trace, world, cfg, iters=None):

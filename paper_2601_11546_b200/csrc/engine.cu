@@ -762,16 +762,32 @@ struct HostTrace {
   long long log_read = 0;
   // one device arena per trace (a cudaMalloc per buffer costs more than the upload itself)
   char* arena = nullptr;
+  void* arena_alloc = nullptr;  // cudaMallocAsync (pool) allocation
   size_t arena_cap = 0, arena_used = 0;
   double* noise_buf = nullptr;  // rs_engine_set_noise
 };
 
 // Reserve the trace's arena: every dalloc below carves from it (256-byte aligned).
+// The arena comes from the device's stream-ordered pool, which keeps freed
+// memory (release threshold = max): re-creating an engine of the same shape
+// reuses it instead of mapping fresh pages (a cudaMalloc/cudaFree round trip
+// of tens of MB costs milliseconds).
+void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 int arena_reserve(HostTrace& h, size_t bytes) {
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, bytes);
-  if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-  h.allocs.push_back(q);
+  cudaError_t e = cudaMallocAsync(&q, bytes, 0);
+  if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+  h.arena_alloc = q;
   h.arena = (char*)q;
   h.arena_cap = bytes;
   h.arena_used = 0;
@@ -1100,6 +1116,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   if (rc) return rc;
   PhaseClock pc;
   RS_CUDA(cudaSetDevice(device));
+  keep_pool(device);
   pc.mark("cudaSetDevice");
   rs_engine* e = new rs_engine();
   e->device = device;
@@ -1346,16 +1363,23 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
   const HostTrace& h = e->traces[t];
   const int R = h.dev.R, N = h.dev.N;
   RS_CUDA(cudaSetDevice(e->device));
+  if (h.row_src.empty() && !generated && !prefilled && !priority) {
+    // identity order, completion only: copy the int32 column into the upper half of the
+    // caller's int64 buffer, then widen in place front to back (element k is read from
+    // byte 4N + 4k before byte 8k overwrites it)
+    if (N) {
+      int32_t* stage = reinterpret_cast<int32_t*>(completion_iter) + N;
+      RS_CUDA(cudaMemcpy(stage, h.dev.comp, (size_t)N * 4, cudaMemcpyDeviceToHost));
+      for (int k = 0; k < N; ++k) completion_iter[k] = stage[k];
+    }
+    return RS_OK;
+  }
   std::vector<int> gen(generated ? N : 0), comp(completion_iter ? N : 0);
   std::vector<unsigned char> tab(h.rq_host.size());
   if (N && generated) RS_CUDA(cudaMemcpy(gen.data(), h.dev.gen, N * 4, cudaMemcpyDeviceToHost));
   if (N && completion_iter) RS_CUDA(cudaMemcpy(comp.data(), h.dev.comp, N * 4, cudaMemcpyDeviceToHost));
   if (prefilled || priority) RS_CUDA(cudaMemcpy(tab.data(), h.dev.rq_global, tab.size(), cudaMemcpyDeviceToHost));
   const RqView v = rq_carve(tab.data(), R);
-  if (h.row_src.empty() && !generated && !prefilled && !priority) {  // identity order, completion only
-    for (int k = 0; k < N; ++k) completion_iter[k] = comp[k];
-    return RS_OK;
-  }
   for (int a = 0; a < R; ++a) {
     const int lo = h.off[a], hi = h.off[a + 1];
     const int qa = (prefilled || priority) ? v.q[a] : 0;
@@ -1379,6 +1403,7 @@ void rs_engine_destroy(rs_engine* e) {
   if (e->d_peers) cudaFree(e->d_peers);
   for (auto& h : e->traces) {
     for (void* p : h.allocs) cudaFree(p);
+    if (h.arena_alloc) cudaFreeAsync(h.arena_alloc, 0);
     if (h.noise_buf) cudaFree(h.noise_buf);
   }
   if (e->d_traces) cudaFree(e->d_traces);

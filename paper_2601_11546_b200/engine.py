@@ -341,10 +341,11 @@ class Engine:
         order = np.lexsort((c.rel_id, c.arrival))
         admitted = np.zeros(c.num_relqueries, bool)
         admitted[order[: st.admitted]] = True
-        ledgers = {}
         rid, av, fv, lv, dv = (c.rel_id.tolist(), arrival.tolist(), fps.tolist(), lpe.tolist(), lde.tolist())
-        for i in order[: st.admitted].tolist():
-            ledgers[rid[i]] = TimestampLedger(av[i], _opt(fv[i]), _opt(lv[i]), _opt(dv[i]))
+        # NaN (x != x) -> None: the reference's unset timestamps
+        ledgers = {rid[i]: TimestampLedger(av[i], None if fv[i] != fv[i] else fv[i],
+                                           None if lv[i] != lv[i] else lv[i], None if dv[i] != dv[i] else dv[i])
+                   for i in order[: st.admitted].tolist()}
         recs = (np.concatenate(self._records) if self._records
                 else np.zeros(0, _abi.ITER_RECORD_DTYPE))
         log = _DecisionLog(recs if self.config.log_decisions else recs[:0])
