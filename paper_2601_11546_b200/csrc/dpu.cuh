@@ -841,8 +841,9 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
         if (uw > cfg.tau) rq.prio[a] = 0.0;
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
+  // (every estimating path above ends with a barrier: the waiting order sees the new values)
 }
 
 }  // namespace rsd

@@ -63,15 +63,15 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
 
   // ---- A: termination + admission (engine.py:375-380, 243-269)
   if (tid == 0) {
-    S.go = 1;
+    S.go_admit = 1;
     if (c.live == 0 && c.n_admitted == T.R) {
       c.status = RS_OK;
-      S.go = 0;
+      S.go_admit = 0;
     } else if (c.iteration >= cfg.iteration_limit) {
       c.status = RS_EABORT_LIMIT;
-      S.go = 0;
+      S.go_admit = 0;
     } else if (cfg.noise_sigma > 0 && c.n_batch >= T.noise_n) {
-      S.go = 0;  // out of noise draws: end the launch, still running (the host appends more)
+      S.go_admit = 0;  // out of noise draws: end the launch, still running (the host appends more)
     } else {
       int a = c.n_admitted;
       const int a0 = a;
@@ -86,7 +86,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
   }
   __syncthreads();
-  if (!S.go) return false;
+  if (!S.go_admit) return false;
   phase_mark(c, 0);
 
   // ---- B: priorities.  fcfs: 0.0; sp: static_relquery_prio, both set at
@@ -567,7 +567,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     c.iteration++;
   }
   phase_mark(c, 4);
-  __syncthreads();
+  // no closing barrier: the next admission (thread 0) touches nothing the other threads
+  // still read here (its flag is S.go_admit, not the execution phase's S.go)
   return true;
 }
 

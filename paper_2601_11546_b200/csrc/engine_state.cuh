@@ -180,6 +180,7 @@ struct Shared {
   JumpEntry jt[kJumpBits];
   JumpEntry jstep[32];  // (A^k, C_k) for k = 1..32 steps
   int go, action;
+  int go_admit;  // phase A's continue flag (separate from `go`: no barrier closes an iteration)
   int new_lo, new_hi;
   int head, W, taken, J;
   long long utok_sum;
