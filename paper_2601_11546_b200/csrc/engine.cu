@@ -766,6 +766,7 @@ struct HostTrace {
   void* arena_alloc = nullptr;  // cudaMallocAsync (pool) allocation
   size_t arena_cap = 0, arena_used = 0;
   double* noise_buf = nullptr;  // rs_engine_set_noise
+  std::vector<int> zorder;      // every relQuery in the static waiting order
 };
 
 // Reserve the trace's arena: every dalloc below carves from it (256-byte aligned).
@@ -1055,6 +1056,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
         return b;
       };
       std::stable_sort(z.begin(), z.end(), [&](int x, int y) { return bits(x) < bits(y); });
+      h.zorder = z;
       int nz = 0;  // a shard orders only the relQueries it owns (shard.cuh)
       for (long long i = 0; i < R; ++i)
         if (z[i] % shard_world == shard_rank) hv.zl[nz++] = z[i];
@@ -1092,6 +1094,59 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   if (rc) return rc;
 #undef TRY
   return RS_OK;
+}
+
+// Another shard's replica of a built trace (sharded pool, all shards in one
+// engine): the read-only columns (tok, out, first-sight priorities and draw
+// offsets, the RNG jump tables) are shared with `src`; the mutable state gets
+// its own arena, initialised as build_trace does, and the relQuery table its
+// shard's static waiting order.
+static int clone_replica(const HostTrace& src, const rs_config* cfg, const rs_pcg64_state& rng, HostTrace& h,
+                         int shard_world, int shard_rank) {
+  h.pol = src.pol;
+  h.off = src.off;
+  h.rank_of = src.rank_of;
+  h.order = src.order;
+  h.row_src = src.row_src;
+  h.zorder = src.zorder;
+  h.rq_host = src.rq_host;
+  h.dev = src.dev;
+  TraceDev& d = h.dev;
+  const long long R = d.R, N = d.N;
+  int rc;
+#define TRY(x) \
+  if ((rc = (x))) return rc
+  const size_t need = 8 * (size_t)N + 24 * (size_t)R + 8 * (size_t)kMaxJobs * (kSmallMns + 1) + rq_bytes((int)R) +
+                      16 + (size_t)d.fifo_cap * sizeof(FifoEnt) + (size_t)d.log_cap * sizeof(rs_iter_record) +
+                      sizeof(Ctl) + 16 * 256;
+  TRY(arena_reserve(h, need));
+  std::vector<double> nanv(R, NAN);
+  TRY(dalloc(h, &d.fps, R, nanv.data()));
+  TRY(dalloc(h, &d.lpe, R, nanv.data()));
+  TRY(dalloc(h, &d.lde, R, nanv.data()));
+  TRY(dalloc(h, &d.gen, N, nullptr, 0));
+  TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
+  TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
+  {
+    RqView hv = rq_carve(h.rq_host.data(), (int)R);
+    int nz = 0;
+    for (long long i = 0; i < R; ++i)
+      if (h.zorder[i] % shard_world == shard_rank) hv.zl[nz++] = h.zorder[i];
+    d.nzl = nz;
+    d.shard_world = shard_world;
+    d.shard_rank = shard_rank;
+    TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
+  }
+  TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
+  if (d.log_cap > 0) TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
+  Ctl* ctl = (Ctl*)calloc(1, sizeof(Ctl));
+  if (!ctl) return fail(RS_ENOMEM, "host alloc");
+  ctl->status = RS_RUNNING;
+  ctl->rng = rng;
+  rc = dalloc(h, &d.ctl, 1, ctl);
+  free(ctl);
+#undef TRY
+  return rc;
 }
 
 static int upload_traces(rs_engine* e) {
@@ -1132,7 +1187,10 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   };
   for (int t = 0; t < n_traces; ++t) {
     const int srank = shard_world == 1 ? 0 : (shard_rank < 0 ? t : shard_rank);
-    rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t], shard_world, srank);
+    if (shard_world > 1 && shard_rank < 0 && t > 0)  // another shard of the same pool on this device
+      rc = clone_replica(e->traces[0], cfg, rng[t], e->traces[t], shard_world, srank);
+    else
+      rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t], shard_world, srank);
     if (rc) return bail(rc);
   }
   if (shard_world > 1) {  // mailboxes (shard.cuh); zeroed: sequence numbers start at 1
