@@ -446,94 +446,113 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
 // must advance as the reference's choice() calls would consume it; draws are
 // replayed in parallel (jump-ahead) just to detect Lemire rejections, which
 // change how many values are consumed (then: sequential replay).
+// The generator state after k more next32 values (numpy's half-word buffer:
+// a buffered value is consumed first; an odd count leaves a high half buffered).
+__device__ __forceinline__ rs_pcg64_state advance32(rs_pcg64_state r, long long k, const JumpEntry* jt) {
+  if (k <= 0) return r;
+  if (r.has_uint32) {
+    r.has_uint32 = 0;
+    if (--k == 0) return r;
+  }
+  const U128 s1 = pcg_jump(U128{r.state_hi, r.state_lo}, (unsigned long long)((k + 1) >> 1), jt);
+  r.state_hi = s1.hi;
+  r.state_lo = s1.lo;
+  if (k & 1) {
+    r.has_uint32 = 1;
+    r.uinteger = (uint32_t)(pcg_output(s1) >> 32);
+  }
+  return r;
+}
+
 __device__ void first_sight(const Params& P, const TraceDev& T, Shared& S, int lo, int hi) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const int tid = threadIdx.x;
   const int Ssz = (int)P.cfg.sample_size;
   for (int a = lo + tid; a < hi; a += kThreads) rq.prio[a] = T.fsprio[a];
-  const long long P0 = T.fs_doff[lo];
-  const long long D = T.fs_doff[hi] - P0;
-  if (tid == 0) S.rng_reject = 0;
-  __syncthreads();
-  const unsigned h0 = c.rng.has_uint32;
-  const U128 s0{c.rng.state_hi, c.rng.state_lo};
-  const long long ppt = (D + kThreads - 1) / kThreads;
-  long long p = (long long)tid * ppt;
-  const long long pend = p + ppt < D ? p + ppt : D;
-  if (p < pend) {
-    // owner of position p: the last arrival with fs_doff <= P0 + p
-    int l = lo, r = hi;  // invariant: fs_doff[l] - P0 <= p < fs_doff[r] - P0
-    while (r - l > 1) {
-      const int mid = (l + r) >> 1;
-      if (T.fs_doff[mid] - P0 <= p) l = mid;
-      else r = mid;
-    }
-    int e = l;
-    U128 st = s0;
-    uint64_t out = 0;
-    int half = 0;
-    bool fresh = true, rej = false;
-    for (; p < pend; ++p) {
-      uint32_t v;
-      if (h0 && p == 0) {
-        v = c.rng.uinteger;
-      } else {
-        if (fresh) {
-          const long long pp = p - (long long)h0;
-          st = pcg_jump(s0, (unsigned long long)(pp >> 1) + 1, S.jt);
-          out = pcg_output(st);
-          half = (int)(pp & 1);
-          fresh = false;
-        } else if (half == 0) {
-          half = 1;
+  // Replay the draws of arrivals [e_lo, hi) in parallel, each thread a run of
+  // stream positions, assuming no Lemire rejection.  A rejection consumes an
+  // extra value and shifts every later draw: the arrival that hit the first
+  // one is replayed exactly by thread 0 and the parallel replay restarts after it.
+  int e_lo = lo;
+  while (e_lo < hi) {
+    const long long P0 = T.fs_doff[e_lo];
+    const long long D = T.fs_doff[hi] - P0;
+    if (tid == 0) S.rej_pos = ~0ULL;
+    __syncthreads();
+    const unsigned h0 = c.rng.has_uint32;
+    const U128 s0{c.rng.state_hi, c.rng.state_lo};
+    const long long ppt = (D + kThreads - 1) / kThreads;
+    long long p = (long long)tid * ppt;
+    const long long pend = p + ppt < D ? p + ppt : D;
+    if (p < pend) {
+      // owner of position p: the last arrival with fs_doff <= P0 + p
+      int l = e_lo, r = hi;  // invariant: fs_doff[l] - P0 <= p < fs_doff[r] - P0
+      while (r - l > 1) {
+        const int mid = (l + r) >> 1;
+        if (T.fs_doff[mid] - P0 <= p) l = mid;
+        else r = mid;
+      }
+      int e = l;
+      U128 st = s0;
+      uint64_t out = 0;
+      int half = 0;
+      bool fresh = true;
+      for (; p < pend; ++p) {
+        uint32_t v;
+        if (h0 && p == 0) {
+          v = c.rng.uinteger;
         } else {
-          st = add128(mul128(S.jt[0].a, st), S.jt[0].c);
-          out = pcg_output(st);
-          half = 0;
+          if (fresh) {
+            const long long pp = p - (long long)h0;
+            st = pcg_jump(s0, (unsigned long long)(pp >> 1) + 1, S.jt);
+            out = pcg_output(st);
+            half = (int)(pp & 1);
+            fresh = false;
+          } else if (half == 0) {
+            half = 1;
+          } else {
+            st = add128(mul128(S.jt[0].a, st), S.jt[0].c);
+            out = pcg_output(st);
+            half = 0;
+          }
+          v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
         }
-        v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
+        while (T.fs_doff[e + 1] - P0 <= p) ++e;
+        const int d = (int)(p - (T.fs_doff[e] - P0));
+        const uint32_t n = (uint32_t)(rq.off[e + 1] - rq.off[e]);
+        const uint32_t bound = d < Ssz ? n - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+        const uint32_t excl = bound + 1u;
+        const uint32_t left = (uint32_t)((uint64_t)v * excl);
+        if (left < excl && left < (0xFFFFFFFFu - bound) % excl) {  // Lemire rejection
+          atomicMin(&S.rej_pos, (unsigned long long)p);
+          break;
+        }
       }
-      while (T.fs_doff[e + 1] - P0 <= p) ++e;
-      const int d = (int)(p - (T.fs_doff[e] - P0));
-      const uint32_t n = (uint32_t)(rq.off[e + 1] - rq.off[e]);
-      const uint32_t bound = d < Ssz ? n - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
-      const uint32_t excl = bound + 1u;
-      const uint32_t left = (uint32_t)((uint64_t)v * excl);
-      if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;
     }
-    if (rej) S.rng_reject = 1;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (S.rng_reject) {  // cold path: exact sequential consumption
-      Pcg64 g = Pcg64::from(c.rng);
-      for (int a = lo; a < hi; ++a) {
-        const uint32_t n = (uint32_t)(rq.off[a + 1] - rq.off[a]);
-        if (n > (uint32_t)Ssz) {
-          uint32_t idx[kMaxSample];
-          choice_floyd(g, n, (uint32_t)Ssz, idx);
-        }
+    __syncthreads();
+    const unsigned long long rp = S.rej_pos;
+    if (rp == ~0ULL) {  // no rejection: consume the D values
+      if (tid == 0) c.rng = advance32(c.rng, D, S.jt);
+      break;
+    }
+    if (tid == 0) {  // cold path: the rejecting arrival's choice() call, exactly
+      int l = e_lo, r = hi;
+      while (r - l > 1) {
+        const int mid = (l + r) >> 1;
+        if ((unsigned long long)(T.fs_doff[mid] - P0) <= rp) l = mid;
+        else r = mid;
       }
+      Pcg64 g = Pcg64::from(advance32(c.rng, T.fs_doff[l] - P0, S.jt));
+      uint32_t idx[kMaxSample];
+      choice_floyd(g, (uint32_t)(rq.off[l + 1] - rq.off[l]), (uint32_t)Ssz, idx);
       c.rng = g.to();
-    } else if (D > 0) {
-      const long long cnt = D - (long long)h0;
-      if (cnt <= 0) {
-        c.rng.has_uint32 = 0;
-      } else {
-        const U128 s1 = pcg_jump(s0, (unsigned long long)((cnt + 1) >> 1), S.jt);
-        c.rng.state_hi = s1.hi;
-        c.rng.state_lo = s1.lo;
-        if (cnt & 1) {
-          c.rng.has_uint32 = 1;
-          c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);
-        } else {
-          c.rng.has_uint32 = 0;
-        }
-      }
+      S.new_lo_rs = l + 1;
     }
-    c.alg_bytes += 12LL * (hi - lo);  // precomputed priority + draw offset per arrival
+    __syncthreads();
+    e_lo = S.new_lo_rs;
   }
+  if (tid == 0) c.alg_bytes += 12LL * (hi - lo);  // precomputed priority + draw offset per arrival
   __syncthreads();
 }
 

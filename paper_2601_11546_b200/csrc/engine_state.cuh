@@ -201,6 +201,8 @@ struct Shared {
   double est_ratio[kEstBatch];
   PrefixSummary est_ps[kEstBatch];
   int rng_reject;
+  unsigned long long rej_pos;  // first-sight replay: first stream position with a Lemire rejection
+  int new_lo_rs;               // ... and the arrival its parallel replay restarts at
   // batched prefill eviction
   int fp_bad, fp_popped, fp_par, fp_cut;
   long long fp_rem;
