@@ -73,11 +73,23 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     } else if (cfg.noise_sigma > 0 && c.n_batch >= T.noise_n) {
       S.go_admit = 0;  // out of noise draws: end the launch, still running (the host appends more)
     } else {
-      int a = c.n_admitted;
-      const int a0 = a;
-      while (a < T.R && rq.arrival[a] <= c.clock) {
-        c.n_wait += rq.off[a + 1] > rq.off[a];  // a waiting entry iff it has rows
-        ++a;
+      // admission ranks are sorted by arrival: gallop, then bisect, to the first arrival > clock
+      const int a0 = c.n_admitted;
+      int a = a0;
+      if (a < T.R && rq.arrival[a] <= c.clock) {
+        int lo_a = a, step = 1;  // arrival[lo_a] <= clock
+        while (a + step < T.R && rq.arrival[a + step] <= c.clock) {
+          lo_a = a + step;
+          step <<= 1;
+        }
+        int hi_a = a + step < T.R ? a + step : T.R;  // arrival[hi_a] > clock, or the end
+        while (hi_a - lo_a > 1) {
+          const int mid = (lo_a + hi_a) >> 1;
+          if (rq.arrival[mid] <= c.clock) lo_a = mid;
+          else hi_a = mid;
+        }
+        a = hi_a;
+        c.n_wait += T.ne_pref[a] - T.ne_pref[a0];  // waiting entries: the arrivals with rows
       }
       c.live += a - a0;
       c.n_admitted = a;
@@ -979,7 +991,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       while (lc < log_cap) lc <<= 1;
     }
     const size_t need = 16 * (size_t)N + 24 * (size_t)R + 8 * (size_t)kMaxJobs * (kSmallMns + 1) +
-                        8 * (size_t)(R + 1) + 8 * (size_t)R + 4 * (size_t)(R + 1) + 4 * (size_t)R +
+                        8 * (size_t)(R + 1) + 8 * (size_t)R + 8 * (size_t)(R + 1) + 4 * (size_t)R +
                         rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
                         (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
                         32 * 256;
@@ -996,6 +1008,11 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
   TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
+  {
+    std::vector<int> nep(R + 1, 0);  // relQueries with rows among admission ranks [0, a)
+    for (long long a = 0; a < R; ++a) nep[a + 1] = nep[a] + (off[a + 1] > off[a]);
+    TRY(dalloc(h, (int**)&d.ne_pref, R + 1, nep.data()));
+  }
   {
     pc.mark("row uploads");
     // first sight (dpu.cuh first_sight): draw-count prefix on the host, the

@@ -144,6 +144,7 @@ struct TraceDev {
   double* term_spill;     // [kMaxJobs * (kSmallMns + 1)] PEM terms beyond kJobTerms per segment
   const double* fsprio;   // [R] first-sight priority (static: no prefilled row, cold chain, ratio 1.0)
   const long long* fs_doff;  // [R+1] prefix of first-sight draw counts (2S-1 per relQuery larger than S)
+  const int* ne_pref;        // [R+1] prefix count of relQueries with rows (waiting entries at admission)
   int fast;                  // engine_kernel<true> applies (see host)
   int nzl;                   // entries of rq.zl (this shard's relQueries)
   int shard_world, shard_rank;  // sharded pool: relQuery a is owned by shard a % world (1, 0: unsharded)
