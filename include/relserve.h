@@ -263,6 +263,25 @@ int rs_pem_batch(int64_t n_sets, const int64_t* item_off, const int64_t* utok,
                  const rs_cost_model* model, double* values_out, int32_t device);
 
 /*
+ * The Adaptive Batch Arranger for given candidates (the engine's device code):
+ * project_delta(prefill, output_limit_p, running, W, model) (arranger.py:115-143)
+ * when both candidates are non-empty and m_plus <= m_minus, then decide_next
+ * (arranger.py:146-179); fcfs/sp decide prefill-first (engine.py:387-395).
+ * Running side: the n_run DISTINCT relQueries of the decode candidate (rel_id,
+ * output_limit; any order -- sorted by rel_id on the device as engine.py:406-408
+ * does), d_min_rel_id = rel_id of the first running request with the minimum
+ * priority m_plus.  Prefill side: n_prefill requests with prefill_utok
+ * uncached tokens of relQuery prefill_rel_id, priority m_minus.  An empty
+ * candidate has n = 0 (its m is ignored).  n_waiting = len(waiting).  Writes
+ * action, kase, m_plus, m_minus, delta_plus/minus/total (NaN = None),
+ * n_waiting and batch_n of *out.  Host buffers; synchronous.
+ */
+int rs_arrange(int32_t n_run, const int64_t* run_rel_id, const int64_t* run_output_limit, int64_t d_min_rel_id,
+               int32_t n_prefill, int64_t prefill_utok, int64_t prefill_rel_id, int64_t prefill_output_limit,
+               double m_plus, double m_minus, int64_t n_waiting, int32_t policy, const rs_cost_model* model,
+               int32_t device, rs_iter_record* out);
+
+/*
  * numpy Generator.choice(n, k, replace=False) replay for a sequence of calls
  * (prefix_cache.py:157-158): call c draws k[c] of n[c] (k < n, Floyd path),
  * writing the k[c] indices at idx_out[off] (off = running sum of k).  The

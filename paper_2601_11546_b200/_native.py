@@ -74,6 +74,10 @@ def lib():
     L.rs_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p]
     L.rs_ipc_open_handle.restype = C.c_int
     L.rs_ipc_open_handle.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.rs_arrange.restype = C.c_int
+    L.rs_arrange.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
+                             C.c_int64, C.c_double, C.c_double, C.c_int64, C.c_int32, C.POINTER(_abi.CostModel),
+                             C.c_int32, C.c_void_p]
     L.rs_engine_set_noise.restype = C.c_int
     L.rs_engine_set_noise.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]
     L.rs_ipc_close.restype = C.c_int
@@ -88,7 +92,7 @@ EXPORTED_SYMBOLS = (
     "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_destroy",
     "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
-    "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise",
+    "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange",
 )
 
 
@@ -246,3 +250,20 @@ def choice_sequence(state: _abi.Pcg64State, ns, ks, device=0) -> np.ndarray:
     _check(lib().rs_choice_sequence(C.byref(state), len(ns), ns.ctypes.data, ks.ctypes.data,
                                     out.ctypes.data, device))
     return out[: int(ks.sum())]
+
+
+def arrange(running, d_min_rel_id, prefill_n, prefill_utok, prefill_rel_id, prefill_output_limit, m_plus, m_minus,
+            n_waiting, policy, model, device=0) -> np.ndarray:
+    """The device arranger (include/relserve.h rs_arrange).  running: [(rel_id, output_limit)] of the
+    decode candidate's distinct relQueries.  Returns one rs_iter_record (NaN = None)."""
+    rel = np.ascontiguousarray([r for r, _ in running], np.int64)
+    ol = np.ascontiguousarray([o for _, o in running], np.int64)
+    out = np.zeros(1, _abi.ITER_RECORD_DTYPE)
+    cm = _abi.CostModel(model.alpha_p, model.beta_p, model.alpha_d, model.beta_d)
+    nan = float("nan")
+    _check(lib().rs_arrange(len(rel), rel.ctypes.data if len(rel) else None, ol.ctypes.data if len(ol) else None,
+                            int(d_min_rel_id), int(prefill_n), int(prefill_utok), int(prefill_rel_id),
+                            int(prefill_output_limit), nan if m_plus is None else float(m_plus),
+                            nan if m_minus is None else float(m_minus), int(n_waiting), _abi.POLICY_IDS[policy],
+                            C.byref(cm), device, out.ctypes.data))
+    return out[0]

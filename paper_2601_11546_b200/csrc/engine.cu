@@ -44,6 +44,73 @@ namespace rsd {
 // One scheduler iteration (all threads).  Returns false when the trace stopped.
 // ---------------------------------------------------------------------------
 
+// The Adaptive Batch Arranger's decision, thread 0 (engine.py:387-433):
+// project_delta (arranger.py:115-143) when both candidates are non-empty and
+// m+ <= m-, evaluated left to right in fp64 exactly as written, then
+// decide_next (arranger.py:146-179); fcfs/sp are prefill-first
+// (engine.py:387-395).  ol(i) is the output limit of the i-th distinct
+// running relQuery in rel_id order (engine.py:406-408); internal = the first
+// running row attaining m+ belongs to the prefill candidate's relQuery.
+// Outputs follow rs_iter_record: NaN where the reference logs None.
+template <class OL>
+__device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_first, int force, bool has_p,
+                                        bool has_d, bool internal, double m_plus, double m_minus, long long utok_sum,
+                                        int n_p, long long ol_p, int n_dist, const OL& ol, long long W, int& action,
+                                        int& kase, double& mp, double& mmn, double& dp, double& dm, double& dt) {
+  dp = dm = dt = __longlong_as_double(0x7FF8000000000000LL);
+  mp = m_plus;
+  mmn = m_minus;
+  if (prefill_first) {
+    kase = RS_CASE_FORCED;
+    if (has_p) action = RS_ACTION_PREFILL;
+    else if (has_d) action = RS_ACTION_DECODE;
+    else {
+      action = RS_ACTION_IDLE;
+      mp = mmn = dp;
+    }
+    return;
+  }
+  double ddp = 0, ddm = 0, ddt = 0;
+  if (has_p && has_d && m_plus <= m_minus) {  // project_delta
+    const double l_prefill = __dadd_rn(__dmul_rn(m.alpha_p, (double)utok_sum), m.beta_p);
+    ddp = __dmul_rn(l_prefill, (double)n_dist);
+    long long max_ol = 0;
+    const double adn = __dmul_rn(m.alpha_d, (double)n_p);
+    for (int i = 0; i < n_dist; ++i) {
+      const long long o = ol(i);
+      ddp = __dadd_rn(ddp, __dmul_rn(adn, (double)(o < ol_p ? o : ol_p)));
+      max_ol = o > max_ol ? o : max_ol;
+    }
+    ddm = -__dmul_rn(__dmul_rn((double)W, m.beta_d), (double)(ol_p < max_ol ? ol_p : max_ol));
+    ddt = __dadd_rn(ddp, ddm);
+  }
+  if (!has_p && !has_d) {
+    action = RS_ACTION_IDLE;
+    kase = RS_CASE_FORCED;
+    mp = mmn = dp;
+  } else if (!has_d) {
+    action = RS_ACTION_PREFILL;
+    kase = RS_CASE_FORCED;
+  } else if (!has_p) {
+    action = RS_ACTION_DECODE;
+    kase = RS_CASE_FORCED;
+  } else if (internal) {
+    action = RS_ACTION_PREFILL;
+    kase = RS_CASE_INTERNAL;
+  } else if (m_plus > m_minus) {
+    action = RS_ACTION_PREFILL;
+    kase = RS_CASE_PREEMPT;
+  } else {
+    kase = RS_CASE_TRANSITIONAL;
+    dp = ddp;
+    dm = ddm;
+    dt = ddt;
+    if (force == 1) action = RS_ACTION_PREFILL;
+    else if (force == 2) action = RS_ACTION_DECODE;
+    else action = (ddt < 0) ? RS_ACTION_PREFILL : RS_ACTION_DECODE;
+  }
+}
+
 // _world_duration (engine.py:310-313): base * (1 + sigma * z), clamped at 0,
 // z = the n-th standard normal of the engine's noise stream (one per executed batch)
 __device__ __forceinline__ double world_duration(const Params& P, const TraceDev& T, long long n, double base) {
@@ -314,61 +381,11 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   }
   if (tid == 0) {
     int action, kase;
-    double dp = qnan(), dm = qnan(), dt = qnan();
-    double mp = S.m_plus, mmn = S.m_minus;
-    if (P.prefill_first) {
-      kase = RS_CASE_FORCED;
-      if (has_p) action = RS_ACTION_PREFILL;
-      else if (has_d) action = RS_ACTION_DECODE;
-      else {
-        action = RS_ACTION_IDLE;
-        mp = mmn = qnan();
-      }
-    } else {
-      double ddp = 0, ddm = 0, ddt = 0;
-      if (need_proj) {  // project_delta (arranger.py:115-143), left-to-right fp64
-        const rs_cost_model& m = P.pol;
-        const double l_prefill = __dadd_rn(__dmul_rn(m.alpha_p, (double)S.utok_sum), m.beta_p);
-        const long long ol_p = rq.ol[S.head];
-        ddp = __dmul_rn(l_prefill, (double)S.n_dist);
-        long long max_ol = 0;
-        const double adn = __dmul_rn(m.alpha_d, (double)S.taken);
-        for (int i = 0; i < S.n_dist; ++i) {
-          const long long ol = rq.ol[S.sorted_dist[i]];
-          const long long mn = ol < ol_p ? ol : ol_p;
-          ddp = __dadd_rn(ddp, __dmul_rn(adn, (double)mn));
-          max_ol = ol > max_ol ? ol : max_ol;
-        }
-        const long long mn = ol_p < max_ol ? ol_p : max_ol;
-        ddm = -__dmul_rn(__dmul_rn((double)S.W, m.beta_d), (double)mn);
-        ddt = __dadd_rn(ddp, ddm);
-      }
-      if (!has_p && !has_d) {
-        action = RS_ACTION_IDLE;
-        kase = RS_CASE_FORCED;
-        mp = mmn = qnan();
-      } else if (!has_d) {
-        action = RS_ACTION_PREFILL;
-        kase = RS_CASE_FORCED;
-      } else if (!has_p) {
-        action = RS_ACTION_DECODE;
-        kase = RS_CASE_FORCED;
-      } else if (S.dmin_slot == S.head) {
-        action = RS_ACTION_PREFILL;
-        kase = RS_CASE_INTERNAL;
-      } else if (S.m_plus > S.m_minus) {
-        action = RS_ACTION_PREFILL;
-        kase = RS_CASE_PREEMPT;
-      } else {
-        kase = RS_CASE_TRANSITIONAL;
-        dp = ddp;
-        dm = ddm;
-        dt = ddt;
-        if (P.force == 1) action = RS_ACTION_PREFILL;
-        else if (P.force == 2) action = RS_ACTION_DECODE;
-        else action = (ddt < 0) ? RS_ACTION_PREFILL : RS_ACTION_DECODE;
-      }
-    }
+    double dp, dm, dt, mp, mmn;
+    const int* sd = S.sorted_dist;
+    arrange(P.pol, P.prefill_first, P.force, has_p, has_d, S.dmin_slot == S.head, S.m_plus, S.m_minus, S.utok_sum,
+            S.taken, need_proj ? rq.ol[S.head] : 0, need_proj ? S.n_dist : 0, [&](int i) { return (long long)rq.ol[sd[i]]; },
+            S.W, action, kase, mp, mmn, dp, dm, dt);
     S.action = action;
     c.zptr = zptr_new;
     if (cfg.log_decisions && T.log_cap > 0) {
@@ -703,6 +720,37 @@ __global__ void choice_kernel(rs_pcg64_state* st, long long n_calls, const long 
     o += k[c];
   }
   *st = g.to();
+}
+
+// Unit entry point of the arranger (rs_arrange): rank the distinct running
+// relQueries by rel_id as the engine does (engine.py:406-408), then thread 0
+// runs the engine's arrange().
+__global__ void arrange_kernel(int n_run, const long long* run_rel, const long long* run_ol, long long d_min_rel,
+                               int n_p, long long utok_sum, long long p_rel, long long ol_p, double m_plus,
+                               double m_minus, long long W, int prefill_first, int force, rs_cost_model m,
+                               long long* sorted_ol, rs_iter_record* out) {
+  for (int i = threadIdx.x; i < n_run; i += blockDim.x) {
+    int pos = 0;
+    for (int k = 0; k < n_run; ++k) pos += run_rel[k] < run_rel[i];
+    sorted_ol[pos] = run_ol[i];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int action, kase;
+  double mp, mmn, dp, dm, dt;
+  arrange(m, prefill_first, force, n_p > 0, n_run > 0, n_run > 0 && n_p > 0 && d_min_rel == p_rel, m_plus, m_minus,
+          utok_sum, n_p, ol_p, n_run, [&](int i) { return sorted_ol[i]; }, W, action, kase, mp, mmn, dp, dm, dt);
+  rs_iter_record r{};
+  r.m_plus = mp;
+  r.m_minus = mmn;
+  r.delta_plus = dp;
+  r.delta_minus = dm;
+  r.delta_total = dt;
+  r.action = action;
+  r.kase = kase;
+  r.n_waiting = (int)W;
+  r.batch_n = n_p;
+  *out = r;
 }
 
 // First-sight priorities of every relQuery (one warp each, whole grid): PEM
@@ -1548,6 +1596,34 @@ int rs_pem_batch(int64_t n_sets, const int64_t* item_off, const int64_t* utok, c
   cudaFree(d_pre);
   cudaFree(d_out);
   cudaFree(d_segok);
+  return RS_OK;
+}
+
+int rs_arrange(int32_t n_run, const int64_t* run_rel_id, const int64_t* run_output_limit, int64_t d_min_rel_id,
+               int32_t n_prefill, int64_t prefill_utok, int64_t prefill_rel_id, int64_t prefill_output_limit,
+               double m_plus, double m_minus, int64_t n_waiting, int32_t policy, const rs_cost_model* model,
+               int32_t device, rs_iter_record* out) {
+  if (n_run < 0 || n_run > kMaxRun || n_prefill < 0 || !model || !out) return fail(RS_EINVAL, "bad arranger input");
+  if (policy < RS_POLICY_FCFS || policy > RS_POLICY_RELSERVE_DP) return fail(RS_EINVAL, "unknown policy");
+  RS_CUDA(cudaSetDevice(device));
+  long long* d = nullptr;
+  rs_iter_record* d_out = nullptr;
+  const size_t nb = std::max<int32_t>(n_run, 1) * sizeof(long long);
+  RS_CUDA(cudaMalloc(&d, 3 * nb));
+  RS_CUDA(cudaMalloc(&d_out, sizeof(rs_iter_record)));
+  if (n_run) {
+    RS_CUDA(cudaMemcpy(d, run_rel_id, n_run * sizeof(long long), cudaMemcpyHostToDevice));
+    RS_CUDA(cudaMemcpy((char*)d + nb, run_output_limit, n_run * sizeof(long long), cudaMemcpyHostToDevice));
+  }
+  const int prefill_first = policy == RS_POLICY_FCFS || policy == RS_POLICY_SP;
+  const int force = policy == RS_POLICY_RELSERVE_PP ? 1 : policy == RS_POLICY_RELSERVE_DP ? 2 : 0;
+  arrange_kernel<<<1, 32>>>(n_run, d, (long long*)((char*)d + nb), d_min_rel_id, n_prefill, prefill_utok,
+                            prefill_rel_id, prefill_output_limit, m_plus, m_minus, n_waiting, prefill_first, force,
+                            *model, (long long*)((char*)d + 2 * nb), d_out);
+  RS_CUDA(cudaGetLastError());
+  RS_CUDA(cudaMemcpy(out, d_out, sizeof(rs_iter_record), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(d_out);
   return RS_OK;
 }
 
