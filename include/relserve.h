@@ -66,6 +66,9 @@ typedef struct {
   int64_t iteration_limit;
   int32_t log_decisions;          /* record one rs_iter_record per iteration */
   int32_t policy;                 /* RS_POLICY_* */
+  int32_t record_order;           /* parity mode: also record the full waiting order per iteration
+                                     (rs_engine_read_order); needs log_decisions, <= 4096 relQueries */
+  int32_t reserved;
 } rs_config;
 
 /* numpy PCG64 bit-generator state (`Generator.bit_generator.state`). */
@@ -188,6 +191,16 @@ int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* status);
 
 /* Copy decision records [first, first+count) of trace t (must still be in the buffer). */
 int rs_engine_read_log(rs_engine* e, int32_t t, int64_t first, int64_t count, rs_iter_record* out);
+
+/*
+ * Parity mode (cfg.record_order): the whole waiting queue after the priority
+ * update of iterations [first, first+count) (engine.py:277-281: sorted by
+ * (priority, arrival, rel_id)), as trace-order relQuery indices.  Row i of
+ * out has `stride` = num_relqueries entries; its first record.n_waiting are
+ * the queue, the rest -1.  The hot path never sorts: it only needs the head
+ * and the length (a top-1 over a static order).
+ */
+int rs_engine_read_order(rs_engine* e, int32_t t, int64_t first, int64_t count, int32_t* out);
 
 /* Timestamp ledgers per relQuery in trace order; NaN = None (engine.py:52-61). */
 int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* first_prefill_start,

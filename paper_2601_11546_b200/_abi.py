@@ -32,7 +32,7 @@ class Config(C.Structure):
         ("cap", C.c_int64), ("max_num_seqs", C.c_int64), ("max_num_batched_tokens", C.c_int64),
         ("sample_size", C.c_int64), ("tau", C.c_double), ("noise_sigma", C.c_double),
         ("block_size", C.c_int64), ("capacity_blocks", C.c_int64), ("iteration_limit", C.c_int64),
-        ("log_decisions", C.c_int32), ("policy", C.c_int32),
+        ("log_decisions", C.c_int32), ("policy", C.c_int32), ("record_order", C.c_int32), ("reserved", C.c_int32),
     ]
 
 

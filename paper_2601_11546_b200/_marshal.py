@@ -185,9 +185,10 @@ def _py_sum(xs) -> float:
     return float(f)
 
 
-def make_config(cfg, policy: str) -> _abi.Config:
+def make_config(cfg, policy: str, record_order: bool = False) -> _abi.Config:
     cons = cfg.constraints
     return _abi.Config(
+        record_order=int(bool(record_order)),
         cap=cons.cap, max_num_seqs=cons.max_num_seqs,
         max_num_batched_tokens=cons.max_num_batched_tokens,
         sample_size=cfg.sample_size, tau=float(cfg.tau), noise_sigma=float(cfg.noise_sigma),

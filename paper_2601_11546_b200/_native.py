@@ -74,6 +74,8 @@ def lib():
     L.rs_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p]
     L.rs_ipc_open_handle.restype = C.c_int
     L.rs_ipc_open_handle.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.rs_engine_read_order.restype = C.c_int
+    L.rs_engine_read_order.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
     L.rs_arrange.restype = C.c_int
     L.rs_arrange.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
                              C.c_int64, C.c_double, C.c_double, C.c_int64, C.c_int32, C.POINTER(_abi.CostModel),
@@ -93,6 +95,7 @@ EXPORTED_SYMBOLS = (
     "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
     "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange",
+    "rs_engine_read_order",
 )
 
 
@@ -191,6 +194,14 @@ class NativeEngine:
         if count:
             _check(lib().rs_engine_read_log(self.h, t, first, count, out.ctypes.data))
         return out
+
+    def read_order(self, t: int, first: int, count: int, R: int) -> np.ndarray:
+        """Parity mode: the waiting queue of logged iterations [first, first+count), trace-order
+        relQuery indices, one row of R per iteration (-1 past the queue's length)."""
+        out = np.full((count, max(R, 1)), -1, np.int32)
+        if count:
+            _check(lib().rs_engine_read_order(self.h, t, first, count, out.ctypes.data))
+        return out[:, :R]
 
     def read_ledgers(self, t: int, R: int):
         a, b, c, d = (np.zeros(R, np.float64) for _ in range(4))

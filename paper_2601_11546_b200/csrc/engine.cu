@@ -111,6 +111,58 @@ __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_fir
   }
 }
 
+// Parity mode: the whole waiting queue of this iteration sorted by (priority
+// bits, rank) -- the reference's (priority, arrival, rel_id) order,
+// engine.py:175-176, 277-281 -- into order row `row` (all threads; a bitonic
+// sort in shared memory).  Never on the timed path: the engine itself only
+// needs the head and the length.
+__device__ __noinline__ void record_waiting_order(const TraceDev& T, Shared& S, long long row) {
+  Ctl& c = S.c;
+  const RqView rq = S.rq;
+  const int tid = threadIdx.x;
+  int n = 0;
+  for (int a0 = 0; a0 < c.n_admitted; a0 += kThreads) {
+    const int a = a0 + tid;
+    const bool w = a < c.n_admitted && rq.q[a] < rq.off[a + 1] - rq.off[a];
+    int v[1] = {w ? 1 : 0}, tot[1];
+    block_scan32<1>(v, S.s32, tot);
+    if (w) {
+      S.ord.key[n + v[0] - 1] = dbits(rq.prio[a]);
+      S.ord.rank[n + v[0] - 1] = a;
+    }
+    n += tot[0];
+  }
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  for (int i = n + tid; i < n2; i += kThreads) {
+    S.ord.key[i] = ~0ULL;
+    S.ord.rank[i] = 0x7FFFFFFF;
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n2; i += kThreads) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long ki = S.ord.key[i], kl = S.ord.key[l];
+          const int ri = S.ord.rank[i], rl = S.ord.rank[l];
+          const bool gt = ki > kl || (ki == kl && ri > rl);
+          if (gt == ((i & k) == 0)) {
+            S.ord.key[i] = kl;
+            S.ord.key[l] = ki;
+            S.ord.rank[i] = rl;
+            S.ord.rank[l] = ri;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int* out = T.order_buf + (size_t)row * T.R;
+  for (int i = tid; i < T.R; i += kThreads) out[i] = i < n ? S.ord.rank[i] : -1;
+  __syncthreads();
+}
+
 // _world_duration (engine.py:310-313): base * (1 + sigma * z), clamped at 0,
 // z = the n-th standard normal of the engine's noise stream (one per executed batch)
 __device__ __forceinline__ double world_duration(const Params& P, const TraceDev& T, long long n, double base) {
@@ -280,6 +332,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       S.head = head_l;  // read by other threads only after later barriers
     }
   }
+  if (cfg.record_order && T.order_buf) record_waiting_order(T, S, c.n_log & (T.log_cap - 1));
   phase_mark(c, 2);
 
   // ---- D: candidates (engine.py:285-308)
@@ -1148,6 +1201,10 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     d.log_cap = 1;
     while (d.log_cap < log_cap) d.log_cap <<= 1;
     TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
+    if (cfg->record_order) {  // parity mode (outside the arena: it can be large)
+      if (R > kOrderMax) return fail(RS_EUNSUPPORTED, "record_order supports at most 4096 relQueries");
+      TRY(dalloc(h, &d.order_buf, (size_t)d.log_cap * std::max<long long>(R, 1), nullptr, 0xFF));
+    }
   }
   pc.mark("fifo/jump/log");
   Ctl* ctl = (Ctl*)calloc(1, sizeof(Ctl));
@@ -1455,6 +1512,24 @@ int rs_engine_read_log(rs_engine* e, int32_t t, int64_t first, int64_t count, rs
   for (long long i = 0; i < count; ++i) {
     if (out[i].head >= 0) out[i].head = h.order[out[i].head];
     if (out[i].batch_rq >= 0) out[i].batch_rq = h.order[out[i].batch_rq];
+  }
+  return RS_OK;
+}
+
+int rs_engine_read_order(rs_engine* e, int32_t t, int64_t first, int64_t count, int32_t* out) {
+  if (!e || t < 0 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
+  const HostTrace& h = e->traces[t];
+  const TraceDev& d = h.dev;
+  if (!d.order_buf) return fail(RS_EINVAL, "engine created without record_order");
+  if (count <= 0) return RS_OK;
+  if (count > d.log_cap) return fail(RS_EINVAL, "order range exceeds the ring buffer");
+  RS_CUDA(cudaSetDevice(e->device));
+  const long long R = d.R;
+  for (long long i = 0; i < count; ++i) {
+    const long long row = (first + i) & (d.log_cap - 1);
+    RS_CUDA(cudaMemcpy(out + i * R, d.order_buf + row * R, R * sizeof(int), cudaMemcpyDeviceToHost));
+    for (long long k = 0; k < R; ++k)
+      if (out[i * R + k] >= 0) out[i * R + k] = h.order[out[i * R + k]];
   }
   return RS_OK;
 }

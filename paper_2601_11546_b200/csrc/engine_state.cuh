@@ -32,6 +32,7 @@ constexpr int kEstBatch = 128;  // relQueries re-estimated per DPU batch
 constexpr int kDrawBuf = 4096;  // numpy next32 draws staged per DPU batch
 constexpr int kItemBuf = 2048;  // PEM items staged per segment-parallel batch
 constexpr int kPhases = 24;
+constexpr int kOrderMax = 4096;  // parity mode: relQueries whose full waiting order is recorded
 constexpr int kSmallEst = 32;   // DPU fast path: at most this many re-estimated relQueries
 constexpr int kSmallMns = 256;  // ... and max_num_seqs at most this
 constexpr int kMaxJobs = 64;    // ... and at most this many PEM segments
@@ -155,6 +156,7 @@ struct TraceDev {
   long long noise_n;         // ... available (rs_engine_set_noise)
   rs_iter_record* log;
   long long log_cap;
+  int* order_buf;  // parity mode: [log_cap][R] waiting order per logged iteration (ranks)
   Ctl* ctl;
 };
 
@@ -223,6 +225,10 @@ struct Shared {
       int nterm[kMaxJobs];
       int U[kWarps][kSmallMns];  // per-warp utok prefix of the segment it evaluates
     } small;
+    struct {  // parity mode: the waiting queue being sorted
+      unsigned long long key[kOrderMax];
+      int rank[kOrderMax];
+    } ord;
     struct {
       unsigned long long t0[kWin];
       unsigned long long c0[kWin];

@@ -79,6 +79,9 @@ class RunResult:
     records: np.ndarray | None = None
     #: wall time of the whole device run (host view, includes launches/copies)
     device_wall_s: float = 0.0
+    #: parity mode (Engine(record_waiting_order=True)): per iteration, the waiting queue after the
+    #: priority update as trace-order relQuery indices (engine.py:277-281)
+    waiting_orders: list | None = None
 
     @property
     def cache_hit_ratio(self) -> float:
@@ -230,10 +233,13 @@ class Engine:
         stream=None,
         shards: int = 1,
         shard_rank: int = -1,
+        record_waiting_order: bool = False,
     ):
         """shards > 1 runs the sharded pool (include/relserve.h rs_engine_create_sharded):
         shard_rank -1 puts every shard on `device` (one CTA each); shard_rank >= 0 makes this
-        engine one shard of a multi-process group (call connect_shards before run/step)."""
+        engine one shard of a multi-process group (call connect_shards before run/step).
+        record_waiting_order (parity mode): also record the full sorted waiting queue of every
+        iteration (RunResult.waiting_orders); the timed path never sorts."""
         if policy not in POLICIES:
             raise ValueError(f"unknown policy {policy!r}; choose from {POLICIES}")
         self.trace = trace
@@ -254,11 +260,14 @@ class Engine:
         self._m = _marshal.marshal_trace(trace, c.block_size, policy, self.policy_model,
                                          c.sp_priority_fns)
         self._native = _native.NativeEngine(
-            [self._m.view], _marshal.make_config(c, policy), _marshal.make_model(world_model),
+            [self._m.view], _marshal.make_config(c, policy, record_waiting_order and c.log_decisions),
+            _marshal.make_model(world_model),
             _marshal.make_model(self.policy_model), [_marshal.dpu_rng_state(seed)], device,
             log_capacity=self.chunk_iterations if c.log_decisions else 0, shards=shards, rank=shard_rank,
         )
         self.shards, self.shard_rank = shards, shard_rank
+        self._record_order = bool(record_waiting_order and c.log_decisions)
+        self._orders: list[np.ndarray] = []
         # world-model noise (engine.py:198, 310-313): the reference's standard normals, one per
         # executed batch, from the same stream; handed to the device in growing prefixes
         self._noise_rng = None
@@ -306,6 +315,9 @@ class Engine:
             self._extend_noise(len(self._noise))
         if self.config.log_decisions and st.n_log > self._n_read:
             self._records.append(ne.read_log(0, self._n_read, st.n_log - self._n_read))
+            if self._record_order:
+                self._orders.append(ne.read_order(0, self._n_read, st.n_log - self._n_read,
+                                                  self.trace.columns().num_relqueries))
             self._n_read = st.n_log
         self._status = st
         self.iteration = st.iterations
@@ -365,8 +377,14 @@ class Engine:
             dpu_wall_s=self._phase_seconds(st, _DPU_PHASES), aba_wall_s=self._phase_seconds(st, _ABA_PHASES),
             cache_hit_tokens=int(st.cache_hit_tokens),
             cache_miss_tokens=int(st.cache_miss_tokens), completion_iteration=comp, records=recs,
-            device_wall_s=wall,
+            device_wall_s=wall, waiting_orders=self._waiting_orders(recs),
         )
+
+    def _waiting_orders(self, recs):
+        if not self._record_order:
+            return None
+        rows = np.concatenate(self._orders) if self._orders else np.zeros((0, 0), np.int32)
+        return [rows[i, : int(w)] for i, w in enumerate(recs["n_waiting"].tolist())]
 
     @property
     def requests_state(self):

@@ -106,3 +106,30 @@ def test_noise_prefix_refill_matches_reference_golden(chunk, monkeypatch):
     parity.compare_records(res.records, g, trace, f"noise/{chunk}")
     parity.compare_completion(res.completion_iteration, g, trace)
     assert res.sim_duration == g["result"]["sim_duration"]
+
+
+ORDER_GOLDENS = [n for n in golden_names() if any("order" in e for e in load_golden(n)["iters"][:3])]
+
+
+@pytest.mark.parametrize("name", ORDER_GOLDENS)
+def test_device_full_waiting_order_matches_reference(name):
+    """Parity mode: the whole waiting queue (engine.py:277-281, sorted by (priority,
+    arrival, rel_id)) of every iteration equals the reference's, entry for entry."""
+    from paper_2601_11546_b200.engine import Engine, SimulationAborted
+
+    g = load_golden(name)
+    trace, policy, world, cfg, pm, seed = parity.golden_inputs(g)
+    eng = Engine(trace, policy, world, cfg, pm, seed, device=0, record_waiting_order=True)
+    try:
+        res = eng.run()
+    except SimulationAborted:
+        res = eng.result
+    eng.close()
+    rel = trace.columns().rel_id
+    n = 0
+    for e in g["iters"]:
+        if "order" in e:
+            got = [int(rel[i]) for i in res.waiting_orders[e["it"]]]
+            assert got == e["order"], f"{name}: waiting order differs at iteration {e['it']}"
+            n += 1
+    assert n > 0
