@@ -261,6 +261,23 @@ int64_t rs_engine_device_bytes(const rs_engine* e);
 int rs_device_clock_khz(int32_t device);
 
 /* ---------------------------------------------------------------------------
+ * relsim-trace-v1 ingestion (pkg/docs/trace-schema.md; workload.py:324-384):
+ * the counts of a trace file as the columns rs_trace_view points at.  Host
+ * code, no device needed.  Errors (bad schema, size != len(requests),
+ * per-request prefix_len != the relQuery's) return RS_EINVAL with
+ * rs_trace_v1_error() set.
+ * ------------------------------------------------------------------------- */
+typedef struct rs_trace_file rs_trace_file;
+int rs_trace_v1_load(const char* path, rs_trace_file** out);
+int rs_trace_v1_info(const rs_trace_file* f, int64_t* num_relqueries, int64_t* num_requests, double* rate,
+                     int64_t* seed);
+/* rel_id/arrival/output_limit/prefix_len [R], row_off [R+1], tok/out [N], trace (file) order */
+int rs_trace_v1_columns(const rs_trace_file* f, int64_t* rel_id, double* arrival, int32_t* output_limit,
+                        int32_t* prefix_len, int64_t* row_off, int32_t* tok, int32_t* out);
+void rs_trace_v1_free(rs_trace_file* f);
+const char* rs_trace_v1_error(void);
+
+/* ---------------------------------------------------------------------------
  * Unit entry points (parity tests); same device code as the engine.
  * ------------------------------------------------------------------------- */
 

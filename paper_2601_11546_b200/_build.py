@@ -17,7 +17,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 SRC = HERE / "csrc"
 LIB = HERE / "lib" / "librelserve_b200.so"
-SOURCES = [SRC / "engine.cu"]
+SOURCES = [SRC / "engine.cu", SRC / "trace_v1.cpp"]
 HEADERS = sorted(SRC.glob("*.cuh")) + [HERE.parent / "include" / "relserve.h"]
 
 

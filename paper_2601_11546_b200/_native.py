@@ -74,6 +74,15 @@ def lib():
     L.rs_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p]
     L.rs_ipc_open_handle.restype = C.c_int
     L.rs_ipc_open_handle.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.rs_trace_v1_load.restype = C.c_int
+    L.rs_trace_v1_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    L.rs_trace_v1_info.restype = C.c_int
+    L.rs_trace_v1_info.argtypes = [C.c_void_p] + [C.c_void_p] * 4
+    L.rs_trace_v1_columns.restype = C.c_int
+    L.rs_trace_v1_columns.argtypes = [C.c_void_p] + [C.c_void_p] * 7
+    L.rs_trace_v1_free.restype = None
+    L.rs_trace_v1_free.argtypes = [C.c_void_p]
+    L.rs_trace_v1_error.restype = C.c_char_p
     L.rs_engine_read_order.restype = C.c_int
     L.rs_engine_read_order.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
     L.rs_arrange.restype = C.c_int
@@ -95,7 +104,8 @@ EXPORTED_SYMBOLS = (
     "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
     "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange",
-    "rs_engine_read_order",
+    "rs_engine_read_order", "rs_trace_v1_load", "rs_trace_v1_info", "rs_trace_v1_columns", "rs_trace_v1_free",
+    "rs_trace_v1_error",
 )
 
 
@@ -278,3 +288,23 @@ def arrange(running, d_min_rel_id, prefill_n, prefill_utok, prefill_rel_id, pref
                             nan if m_minus is None else float(m_minus), int(n_waiting), _abi.POLICY_IDS[policy],
                             C.byref(cm), device, out.ctypes.data))
     return out[0]
+
+
+def read_trace_v1(path):
+    """relsim-trace-v1 counts via the native reader: (rel_id, arrival, output_limit, prefix_len,
+    row_off, tok, out, rate, seed); ValueError on a malformed file."""
+    L = lib()
+    h = C.c_void_p()
+    if L.rs_trace_v1_load(str(path).encode(), C.byref(h)) != _abi.RS_OK:
+        raise ValueError(L.rs_trace_v1_error().decode())
+    try:
+        R, N, seed = C.c_int64(), C.c_int64(), C.c_int64()
+        rate = C.c_double()
+        L.rs_trace_v1_info(h, C.byref(R), C.byref(N), C.byref(rate), C.byref(seed))
+        R, N = R.value, N.value
+        cols = (np.zeros(R, np.int64), np.zeros(R, np.float64), np.zeros(R, np.int32), np.zeros(R, np.int32),
+                np.zeros(R + 1, np.int64), np.zeros(N, np.int32), np.zeros(N, np.int32))
+        L.rs_trace_v1_columns(h, *(c.ctypes.data for c in cols))
+    finally:
+        L.rs_trace_v1_free(h)
+    return (*cols, rate.value, seed.value)

@@ -446,6 +446,24 @@ def save_trace(trace: ArrivalTrace, path: str | Path) -> None:
 
 
 def load_trace(path: str | Path) -> ArrivalTrace:
+    """Read a relsim-trace-v1 file (workload.py:349-384).  The counts come from the native
+    reader (csrc/trace_v1.cpp) when the library is built, else from the json module."""
+    from . import _native
+
+    path = Path(path)
+    if _native.LIB_PATH.exists():
+        try:
+            rel_id, arrival, limit, plen, row_off, tok, out, rate, seed = _native.read_trace_v1(path)
+        except ValueError as e:
+            raise SchemaError(str(e)) from None
+        cols = TraceColumns(rel_id=rel_id, arrival=arrival, output_limit=limit, prefix_len=plen, row_off=row_off,
+                            tok=tok, out=out, token_seed=int(seed))
+        return ArrivalTrace(rate=rate, seed=int(seed), columns=cols)
+    return load_trace_json(path)
+
+
+def load_trace_json(path: str | Path) -> ArrivalTrace:
+    """load_trace with the json module (the reference's reader, restated on columns)."""
     path = Path(path)
     with path.open() as f:
         header = json.loads(f.readline())

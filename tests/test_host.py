@@ -95,3 +95,40 @@ def test_no_cpu_fallback_without_a_gpu():
     t = generate_trace(TraceConfig(num_relqueries=2, size_range=(1, 3), seed=1))
     with pytest.raises(RuntimeError):
         Engine(t, "relserve", world_preset("opt-13b-like"))
+
+
+def test_native_v1_reader_equals_json_reader(tmp_path):
+    """csrc/trace_v1.cpp reads exactly what the json-module reader does (workload.py:349-384)."""
+    import numpy as np
+
+    from paper_2601_11546_b200 import generate_heavy_tail_trace, load_trace, save_trace
+    from paper_2601_11546_b200.workload import load_trace_json
+
+    for i, tr in enumerate([generate_trace(TraceConfig(num_relqueries=50, size_range=(1, 40), rate=2.5, seed=5)),
+                            generate_heavy_tail_trace(num_relqueries=200, size_range=(1, 99), rate=1e3, seed=2)]):
+        p = tmp_path / f"t{i}.jsonl"
+        save_trace(tr, p)
+        a, b = load_trace(p), load_trace_json(p)
+        assert (a.rate, a.seed) == (b.rate, b.seed)
+        ca, cb = a.columns(), b.columns()
+        for k in ("rel_id", "arrival", "output_limit", "prefix_len", "row_off", "tok", "out"):
+            assert np.array_equal(getattr(ca, k), getattr(cb, k)), k
+        assert ca.token_seed == cb.token_seed
+
+
+@pytest.mark.parametrize("bad", [
+    '{"schema": "relsim-trace-v2", "rate": 1.0, "seed": 0}\n',
+    '{"schema": "relsim-trace-v1", "rate": 1.0, "seed": 0}\n{"rel_id": 0, "arrival_s": 0.5, "size": 2, '
+    '"output_limit": 5, "prefix_len": 8, "requests": [{"tok": 20, "prefix_len": 8, "out": 3}]}\n',
+    '{"schema": "relsim-trace-v1", "rate": 1.0, "seed": 0}\n{"rel_id": 0, "arrival_s": 0.5, "size": 1, '
+    '"output_limit": 5, "prefix_len": 8, "requests": [{"tok": 20, "prefix_len": 9, "out": 3}]}\n',
+    '{"schema": "relsim-trace-v1", "rate": 1.0, "seed": 0}\n{"rel_id": 0, "arrival_s": 0.5, "size": 1, ',
+])
+def test_native_v1_reader_rejects_malformed_files(bad, tmp_path):
+    from paper_2601_11546_b200 import load_trace
+    from paper_2601_11546_b200.workload import SchemaError
+
+    p = tmp_path / "bad.jsonl"
+    p.write_text(bad)
+    with pytest.raises((SchemaError, ValueError)):
+        load_trace(p)
