@@ -308,6 +308,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       PrefixSummary ps{0, 0, 0};
       if (Le > 0 && owne) {
         long long rs = 0, mx = 0;
+#pragma unroll 1
         for (int j = lane; j < c.n_run; j += 32)
           if (c.run_rank[j] == ae) {
             const long long r = ole - c.run_gen[j];
@@ -322,42 +323,38 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     }
   }
   // one PEM segment per warp 1..15 (warp 0 is busy with the RNG above); the
-  // segment's tok loads are issued before the barrier, under the RNG replay
-  const int j_first = warp - 1;
-  int uv[8];
+  // first segment's tok loads are issued before the barrier, under the RNG
+  // replay.  One loop with the barrier in its first pass keeps a single copy
+  // of the job setup in the instruction stream.
   static_assert(kSmallMns <= 8 * 32, "items per lane");
-#define RS_JOB_META(j)                                                               \
-  int e = 0;                                                                         \
-  for (int x = 0; x < n_est; ++x)                                                    \
-    if ((__shfl_sync(kFull, jo, x) <= (j)) & (__shfl_sync(kFull, nj, x) > 0)) e = x;  \
-  const int k = (j) - __shfl_sync(kFull, jo, e);                                     \
-  const int ne = __shfl_sync(kFull, nunp, e);                                        \
-  const int Le = __shfl_sync(kFull, L, e);                                           \
-  const int basee = __shfl_sync(kFull, base, e);                                     \
-  const int ole = __shfl_sync(kFull, ol, e);                                         \
-  const int t0 = k * (int)pm.mns - Le < 0 ? 0 : k * (int)pm.mns - Le;               \
-  const int t1 = (k + 1) * (int)pm.mns - Le < ne ? (k + 1) * (int)pm.mns - Le : ne;  \
-  const int nloc = t1 - t0;                                                          \
-  const int per = (nloc + 31) >> 5;                                                  \
-  const int x0 = lane * per;
-  if (warp > 0 && j_first < J) {
-    RS_JOB_META(j_first)
-    (void)ole;
+  for (int j = warp - 1, first = 1;; j += kWarps - 1, first = 0) {
+    const bool act = warp > 0 && j < J;
+    int e = 0, k = 0, ne = 0, Le = 0, basee = 0, ole = 0, t0 = 0, nloc = 0;
+    int uv[8];
+    if (act) {
+      for (int x = 0; x < n_est; ++x)
+        if ((__shfl_sync(kFull, jo, x) <= j) & (__shfl_sync(kFull, nj, x) > 0)) e = x;
+      k = j - __shfl_sync(kFull, jo, e);
+      ne = __shfl_sync(kFull, nunp, e);
+      Le = __shfl_sync(kFull, L, e);
+      basee = __shfl_sync(kFull, base, e);
+      ole = __shfl_sync(kFull, ol, e);
+      const int mns = (int)pm.mns;
+      t0 = k * mns - Le < 0 ? 0 : k * mns - Le;
+      nloc = ((k + 1) * mns - Le < ne ? (k + 1) * mns - Le : ne) - t0;
+    }
+    // utok prefix of the segment: lane l owns items [l*per, l*per + per), per <= 8 (nloc <= mns)
+    const int per = (nloc + 31) >> 5, x0 = lane * per;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) uv[i] = (i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
-  }
-  __syncthreads();
-  phase_mark(c, 7);
-  for (int j = j_first; warp > 0 && j < J; j += kWarps - 1) {
-    RS_JOB_META(j)
+    for (int i = 0; i < 8; ++i) uv[i] = (act && i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
+    if (first) {
+      __syncthreads();
+      phase_mark(c, 7);
+    }
+    if (!act) break;
     const double ratio = S.est_ratio[e];
     int* Uw = S.small.U[warp];
-    {  // utok prefix of the segment: lane l owns items [l*per, l*per + per), per <= 8
-      // (nloc <= mns <= kSmallMns); one warp scan
-      if (j != j_first) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) uv[i] = (i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
-      }
+    {
       int ls = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -412,7 +409,6 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     }
     __syncwarp();
   }
-#undef RS_JOB_META
   __syncthreads();
   phase_mark(c, 8);
   if (warp == 0 && lane < n_est && own) {  // ordered sums, relQuery by relQuery
@@ -421,16 +417,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       const int cnt = S.small.nterm[j];
       const double* tj = S.small.terms + j * kJobTerms;
       const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
-      const int nsm = cnt < kJobTerms ? cnt : kJobTerms;
-      int i = 0;
-      for (; i + 8 <= nsm; i += 8) {  // loads of 8 terms in flight, then the dependent adds
-        double t[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) t[k] = tj[i + k];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) total = __dadd_rn(total, t[k]);
-      }
-      for (; i < cnt; ++i) total = __dadd_rn(total, i < kJobTerms ? tj[i] : spill[i]);
+      for (int i = 0; i < cnt; ++i) total = __dadd_rn(total, i < kJobTerms ? tj[i] : spill[i]);
     }
     rq.prio[a] = total;
   }
