@@ -105,6 +105,43 @@ __device__ void ratios_sequential(const Params& P, const TraceDev& T, Shared& S,
   c.rng = g.to();
 }
 
+// sample_cache_miss_ratio's sampled rows (prefix_cache.py:157-164): Floyd's
+// set from the K bounded draws of one choice(n, K) call -- a draw equal to an
+// earlier member is replaced by n-K+d; the Fisher-Yates draws after them only
+// permute the set -- and the sum of the sampled rows' tok.
+template <int K>
+__device__ __forceinline__ long long floyd_tok_sum(const int* tok, const unsigned* draws, uint32_t n) {
+  uint32_t idx[K];
+#pragma unroll
+  for (int d = 0; d < K; ++d) {
+    const uint32_t v = draws[d];
+    bool found = false;
+#pragma unroll
+    for (int x = 0; x < d; ++x) found |= idx[x] == v;
+    idx[d] = found ? n - K + d : v;
+  }
+  int t[K];
+#pragma unroll
+  for (int d = 0; d < K; ++d) t[d] = tok[idx[d]];
+  long long sum = 0;
+#pragma unroll
+  for (int d = 0; d < K; ++d) sum += t[d];
+  return sum;
+}
+
+__device__ __noinline__ long long floyd_tok_sum_any(const int* tok, const unsigned* draws, uint32_t n, int K) {
+  uint32_t idx[kMaxSample];
+  long long sum = 0;
+  for (int d = 0; d < K; ++d) {
+    const uint32_t v = draws[d];
+    bool found = false;
+    for (int x = 0; x < d; ++x) found |= idx[x] == v;
+    idx[d] = found ? n - (uint32_t)K + (uint32_t)d : v;
+    sum += tok[idx[d]];
+  }
+  return sum;
+}
+
 // Fast path for the common steady state (few re-estimated relQueries, PEM
 // segments closed by count only, mns <= 256, sample size <= 16): two block
 // barriers in total.
@@ -254,28 +291,12 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
               usum += t - mh;
               tsum += t;
             }
-          } else {
-            uint32_t idx[16];
-#pragma unroll
-            for (int d = 0; d < 16; ++d) {
-              if (d < Ssz) {  // Floyd's set; the shuffle only permutes it
-                const uint32_t j = (uint32_t)(nunp - Ssz + d);
-                const uint32_t v = S.small.draws[doff + d];
-                bool found = false;
-#pragma unroll
-                for (int x = 0; x < 16; ++x) found |= (x < d) && idx[x] == v;
-                idx[d] = found ? j : v;
-              }
-            }
-            long long tv[16];
-#pragma unroll
-            for (int d = 0; d < 16; ++d) tv[d] = d < Ssz ? T.tok[base + (int)idx[d]] : 0;
-#pragma unroll
-            for (int d = 0; d < 16; ++d)
-              if (d < Ssz) {
-                usum += tv[d] - mh;
-                tsum += tv[d];
-              }
+          } else if (Ssz == 8) {  // the default sample size: Floyd's set in registers
+            tsum = floyd_tok_sum<8>(T.tok + base, S.small.draws + doff, (uint32_t)nunp);
+            usum = tsum - 8 * mh;
+          } else {  // other sizes: rolled (the hot path keeps one specialised copy)
+            tsum = floyd_tok_sum_any(T.tok + base, S.small.draws + doff, (uint32_t)nunp, Ssz);
+            usum = tsum - (long long)Ssz * mh;
           }
           ratio = __ddiv_rn((double)usum, (double)tsum);
         }
