@@ -181,8 +181,8 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     mcb = rq.m[a];
     L = rq.nrun[a];  // running rows = the live prefilled rows (prefilled summary)
     dcnt = nunp > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
-    const int tot = nunp + L, mns = (int)pm.mns;  // 32-bit: rows per relQuery < 2^31
-    nj = tot > 0 && own ? (tot + mns - 1) / mns : 0;
+    const unsigned tot = (unsigned)(nunp + L);  // segments = ceil(tot / mns) by multiply-shift (exact: tot < 2^32/mns)
+    nj = tot > 0 && own ? (int)(((unsigned long long)(tot + (unsigned)pm.mns - 1u) * P.mns_magic) >> 32) : 0;
   }
   // draw and PEM-segment offsets in one warp scan: (dcnt << 16) | nj (per-warp
   // totals stay below 2^16: dcnt <= 2*16-1 and nj <= kMaxJobs per kept relQuery)
@@ -438,7 +438,11 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       const int cnt = S.small.nterm[j];
       const double* tj = S.small.terms + j * kJobTerms;
       const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
-      for (int i = 0; i < cnt; ++i) total = __dadd_rn(total, i < kJobTerms ? tj[i] : spill[i]);
+      const int nsm = cnt < kJobTerms ? cnt : kJobTerms;
+#pragma unroll 1
+      for (int i = 0; i < nsm; ++i) total = __dadd_rn(total, tj[i]);
+#pragma unroll 1
+      for (int i = nsm; i < cnt; ++i) total = __dadd_rn(total, spill[i]);  // segments of > 31 sub-batches
     }
     rq.prio[a] = total;
   }

@@ -76,6 +76,7 @@ __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_fir
     ddp = __dmul_rn(l_prefill, (double)n_dist);
     long long max_ol = 0;
     const double adn = __dmul_rn(m.alpha_d, (double)n_p);
+#pragma unroll 1
     for (int i = 0; i < n_dist; ++i) {
       const long long o = ol(i);
       ddp = __dadd_rn(ddp, __dmul_rn(adn, (double)(o < ol_p ? o : ol_p)));
@@ -1355,6 +1356,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   p.force = cfg->policy == RS_POLICY_RELSERVE_PP ? 1 : cfg->policy == RS_POLICY_RELSERVE_DP ? 2 : 0;
   p.prefill_first = cfg->policy == RS_POLICY_FCFS || cfg->policy == RS_POLICY_SP;
   p.zorder = !p.use_dpu || std::isinf(cfg->tau);
+  p.mns_magic = (unsigned long long)(0xFFFFFFFFull / (unsigned long long)cfg->max_num_seqs) + 1;  // see dpu_small
   e->smem = need;
   e->fast = true;
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;

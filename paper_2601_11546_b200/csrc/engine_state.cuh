@@ -170,6 +170,7 @@ struct Params {
   int prefill_first;
   int zorder;  // waiting head from the static order (no starvation override possible)
   long long max_iters;
+  unsigned long long mns_magic;  // floor(2^32 / max_num_seqs) + 1: x / mns == (x * magic) >> 32 for x < 2^32 / mns
 };
 
 struct Shared {
