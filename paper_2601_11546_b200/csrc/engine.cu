@@ -283,6 +283,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         i0 += 32;
       }
       if (P.use_dpu) {  // partially prefilled relQueries with pending rows (this shard's)
+        bool better = false;  // this lane holds one that beats the static-order head
         for (int j = lane; j < c.n_act; j += 32) {
           const int a = c.act[j];
           if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
@@ -290,16 +291,24 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
             if (k < key || (k == key && a < idx)) {
               key = k;
               idx = a;
+              better = true;
             }
           }
         }
+        const unsigned bm = __ballot_sync(kFull, better);
+        if (__popc(bm) == 1) {  // the usual case: the one relQuery being prefilled
+          const int l = __ffs(bm) - 1;
+          key = __shfl_sync(kFull, key, l);
+          idx = __shfl_sync(kFull, idx, l);
+        } else if (bm) {
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-          const unsigned long long ok = __shfl_xor_sync(kFull, key, d);
-          const int oi = __shfl_xor_sync(kFull, idx, d);
-          if (ok < key || (ok == key && oi < idx)) {
-            key = ok;
-            idx = oi;
+          for (int d = 16; d > 0; d >>= 1) {
+            const unsigned long long ok = __shfl_xor_sync(kFull, key, d);
+            const int oi = __shfl_xor_sync(kFull, idx, d);
+            if (ok < key || (ok == key && oi < idx)) {
+              key = ok;
+              idx = oi;
+            }
           }
         }
       }
