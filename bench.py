@@ -128,7 +128,10 @@ def sum_over_ranks(x: float, ws: int, device=None) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region.
+
+    NVML polled from a thread every ~1 ms (the timed regions here last tens of
+    ms, shorter than nvidia-smi's sampling period); nvidia-smi as the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -137,18 +140,48 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.thread = None
+        self.sm, self.mx, self.reasons = [], None, set()
+
+    def _poll(self):
+        import pynvml as N
+
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        flags = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop:
+            self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.reasons.update(k for k, f in flags.items() if r & f)
+            time.sleep(0.001)
 
     def __enter__(self):
+        self.stop = False
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except FileNotFoundError:
-            self.p = None
+            import threading
+
+            import pynvml as N
+
+            N.nvmlInit()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.thread = None
+            try:
+                self.p = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except FileNotFoundError:
+                self.p = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        if self.thread is not None:
+            self.stop = True
+            self.thread.join(timeout=5)
         if self.p is not None:
             self.p.terminate()
             try:
@@ -156,25 +189,22 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.p.kill()
                 out, _ = self.p.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+            for ln in out.splitlines():
+                f = [x.strip() for x in ln.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    self.sm.append(float(f[0]))
+                    self.mx = float(f[1])
+                except ValueError:
+                    continue
+                self.reasons.update(n for n, v in zip(names, f[4:8]) if v.lower().startswith("active"))
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml, 1 ms polling" if self.thread is not None else "nvidia-smi"}
 
 
 def peaks():
