@@ -7,7 +7,9 @@
 //   A  admission                      engine.py:243-269
 //   B  Dynamic Priority Updater       priority.py:261-339        (dpu.cuh)
 //   C  waiting-queue order: top-1     engine.py:277-281: key (prio, arrival,
-//      by CTA argmin + waiting count  rel_id) == (prio bits, admission rank)
+//      over a static order + the      rel_id) == (prio bits, admission rank);
+//      re-estimated relQueries;       sharded pool: allgather of the shards'
+//      waiting count                  heads and priorities (shard.cuh)
 //   D  candidates                     engine.py:285-308, arranger.py:71-112
 //   E  decision + Delta projection    engine.py:387-433, arranger.py:115-179
 //   F  state advance                  engine.py:315-363, 439-448, with the
