@@ -400,11 +400,12 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       const int ub = Uw[bb];
       const int thr = ub - before > pm.mnbt ? ub : before + (int)pm.mnbt;
       int nb = nloc;
-      for (int b2 = bb + 1; b2 < nloc; b2 += 32) {
-        const int x = b2 + lane;
-        const unsigned msk = __ballot_sync(kFull, x < nloc && Uw[x] > thr);
-        if (msk) {
-          nb = b2 + __ffs(msk) - 1;
+      for (int b2 = bb + 1; b2 < nloc; b2 += 64) {  // 64 candidates per round: a sub-batch is ~40-60 rows
+        const int x = b2 + lane, y = x + 32;
+        const bool hx = x < nloc && Uw[x] > thr, hy = y < nloc && Uw[y] > thr;
+        const unsigned mx = __ballot_sync(kFull, hx), my = __ballot_sync(kFull, hy);
+        if (mx | my) {
+          nb = mx ? b2 + __ffs(mx) - 1 : b2 + 32 + __ffs(my) - 1;
           break;
         }
       }
