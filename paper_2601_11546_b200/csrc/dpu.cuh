@@ -394,6 +394,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
     int nterm = 0;
     int bb = 0;
+    int my_end = 0;  // lane l < 32: one past the last row of sub-batch l (its term is computed after the chain)
     while (bb < nloc) {
       // every item is unprefilled, so every sub-batch is non-empty: one p-term each
       const int before = bb ? Uw[bb - 1] : 0;
@@ -409,13 +410,23 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
           break;
         }
       }
-      if (lane == 0) {
+      if (nterm < 32) {
+        if (lane == nterm) my_end = nb;
+      } else if (lane == 0) {  // rare: more than 32 sub-batches in one segment
         const double t = lin(pm.ap, (double)(Uw[nb - 1] - before), pm.bp);
         if (nterm < kJobTerms) tj[nterm] = t;
         else spill[nterm] = t;
       }
       ++nterm;
       bb = nb;
+    }
+    {  // the p-terms of the first 32 sub-batches, one lane each, off the chain's critical path
+      static_assert(kJobTerms >= 32, "terms 0..31 live in shared memory");
+      const int beg = __shfl_up_sync(kFull, my_end, 1);
+      if (lane < nterm && lane < 32) {
+        const int b0 = lane ? beg : 0;
+        tj[lane] = lin(pm.ap, (double)(Uw[my_end - 1] - (b0 ? Uw[b0 - 1] : 0)), pm.bp);
+      }
     }
     if (lane == 0) {
       long long rs = (long long)nloc * ole;
