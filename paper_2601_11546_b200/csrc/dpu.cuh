@@ -211,9 +211,13 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     const unsigned h0 = c.rng.has_uint32;
     const U128 s0{c.rng.state_hi, c.rng.state_lo};
     bool rej = false;
-    if (lane < n_est) {  // owner lookup tables for the (divergent) position loop
-      S.est_doff[lane] = dcnt > 0 ? doff : 0x7FFFFFFF;
-      S.est_nunp[lane] = nunp;
+    {  // owner lookup tables: the k-th relQuery that draws owns positions [k*dper, (k+1)*dper)
+      const unsigned dm = __ballot_sync(kFull, lane < n_est && dcnt > 0);
+      if (lane < n_est) {
+        S.est_doff[lane] = dcnt > 0 ? doff : 0x7FFFFFFF;
+        S.est_nunp[lane] = nunp;
+        if (dcnt > 0) S.est_drawer[__popc(dm & ((1u << lane) - 1u))] = lane;
+      }
     }
     __syncwarp();
     // lane l owns 64-bit output l of each 32-output round: state_{32r+l+1} =
@@ -237,16 +241,16 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
         const int p = (int)h0 + 2 * (r0 + lane) + half;
         if (p < D) {
           const uint32_t v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
-          int e = 0;  // relQuery owning position p: the last one with a draw offset <= p
-          for (int x = 0; x < n_est; ++x)
-            if (S.est_doff[x] <= p) e = x;
-          const int d = p - S.est_doff[e];
-          const uint32_t ne = (uint32_t)S.est_nunp[e];
+          const int kq = (int)(((unsigned)p * P.dper_magic) >> 16);  // p / dper (exact: p < 2^16 / dper)
+          const int d = p - kq * dper;
+          const uint32_t ne = (uint32_t)S.est_nunp[S.est_drawer[kq]];
           const uint32_t bound = d < Ssz ? ne - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
           const uint32_t excl = bound + 1u;
           const uint64_t mm = (uint64_t)v * excl;
           const uint32_t left = (uint32_t)mm;
-          if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;  // Lemire rejection
+          if (left < excl) {  // rare: only then can Lemire reject
+            if (left < (0xFFFFFFFFu - bound) % excl) rej = true;
+          }
           S.small.draws[p] = (uint32_t)(mm >> 32);
         }
       }

@@ -1368,6 +1368,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   p.prefill_first = cfg->policy == RS_POLICY_FCFS || cfg->policy == RS_POLICY_SP;
   p.zorder = !p.use_dpu || std::isinf(cfg->tau);
   p.mns_magic = (unsigned long long)(0xFFFFFFFFull / (unsigned long long)cfg->max_num_seqs) + 1;  // see dpu_small
+  p.dper_magic = (unsigned)(65536 / std::max<long long>(1, 2 * cfg->sample_size - 1)) + 1;
   e->smem = need;
   e->fast = true;
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;

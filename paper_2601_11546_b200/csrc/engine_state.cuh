@@ -171,6 +171,8 @@ struct Params {
   int zorder;  // waiting head from the static order (no starvation override possible)
   long long max_iters;
   unsigned long long mns_magic;  // floor(2^32 / max_num_seqs) + 1: x / mns == (x * magic) >> 32 for x < 2^32 / mns
+  unsigned dper_magic;           // floor(2^16 / (2*sample_size - 1)) + 1: the same for draw positions < 2^16 / dper
+  int pad3;
 };
 
 struct Shared {
@@ -202,6 +204,7 @@ struct Shared {
   int est_rank[kEstBatch], est_off[kEstBatch], est_q[kEstBatch], est_nunp[kEstBatch];
   int est_ol[kEstBatch], est_m[kEstBatch], est_doff[kEstBatch + 1];
   int est_io[kEstBatch + 1], est_jo[kEstBatch + 1];  // PEM item / job offsets
+  int est_drawer[kSmallEst];                          // k-th relQuery with choice() draws (fast path)
   double est_ratio[kEstBatch];
   PrefixSummary est_ps[kEstBatch];
   int rng_reject;
