@@ -357,8 +357,9 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
     int e = 0, k = 0, ne = 0, Le = 0, basee = 0, ole = 0, t0 = 0, nloc = 0;
     int uv[8];
     if (act) {
-      for (int x = 0; x < n_est; ++x)
-        if ((__shfl_sync(kFull, jo, x) <= j) & (__shfl_sync(kFull, nj, x) > 0)) e = x;
+      // the job's relQuery: the last one (lane) whose segments start at or before j
+      const unsigned em = __ballot_sync(kFull, lane < n_est && jo <= j && nj > 0);
+      e = 31 - __clz(em);
       k = j - __shfl_sync(kFull, jo, e);
       ne = __shfl_sync(kFull, nunp, e);
       Le = __shfl_sync(kFull, L, e);
