@@ -212,6 +212,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         }
         a = hi_a;
         c.n_wait += T.ne_pref[a] - T.ne_pref[a0];  // waiting entries: the arrivals with rows
+        c.zh_valid = 0;                             // they may precede the cached static-order head
       }
       c.live += a - a0;
       c.n_admitted = a;
@@ -243,12 +244,18 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   // not-yet-admitted entries fall back to one block reduction over all.
   int head_l;
   int zptr_new = c.zptr;
+  bool z_cache = false;  // this iteration's static-order head can be cached (thread 0, decision block)
+  unsigned long long zkey = ~0ULL;
+  int zidx = 0x7FFFFFFF;
   {
     const int lane = tid & 31;
     unsigned long long key = ~0ULL;
     int idx = 0x7FFFFFFF;
     bool full = !P.zorder;
-    if (P.zorder) {
+    if (P.zorder && c.zh_valid) {  // the static-order head is unchanged since the last scan
+      key = c.zh_key;
+      idx = c.zh_idx;
+    } else if (P.zorder) {
       int i0 = c.zptr;
       bool lead = true;
       for (int round = 0;; ++round) {
@@ -284,6 +291,11 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         }
         i0 += 32;
       }
+    }
+    zkey = key;  // the static-order head
+    zidx = idx;
+    z_cache = P.zorder && !full;
+    if (P.zorder) {
       if (P.use_dpu) {  // partially prefilled relQueries with pending rows (this shard's)
         bool better = false;  // this lane holds one that beats the static-order head
         for (int j = lane; j < c.n_act; j += 32) {
@@ -453,6 +465,11 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
             S.W, action, kase, mp, mmn, dp, dm, dt);
     S.action = action;
     c.zptr = zptr_new;
+    if (z_cache) {  // valid until an admission or a prefill of that relQuery
+      c.zh_key = zkey;
+      c.zh_idx = zidx;
+      c.zh_valid = 1;
+    }
     if (cfg.log_decisions && T.log_cap > 0) {
       c.alg_bytes += sizeof(rs_iter_record);
       rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
@@ -508,6 +525,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
             world_duration(P, T, c.n_batch++, __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p));
         c.n_run = n_run0 + n;
         rq.q[h] = q + n;
+        if (h == c.zh_idx) c.zh_valid = 0;  // the cached static-order head may have left the order
         if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
         if (rq.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
         rq.nrun[h] += n;

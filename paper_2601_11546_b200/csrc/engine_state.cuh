@@ -66,6 +66,8 @@ struct alignas(16) Ctl {
   int n_admitted, live;
   int n_run, n_act;
   int zptr, n_wait;  // static-order scan start (zl entries before it are prefilled); len(waiting)
+  unsigned long long zh_key;  // cached static-order head (priority bits, rank) ...
+  int zh_idx, zh_valid;       // ... valid until an admission or a prefill of that relQuery
   int status, error_detail;
   int cc_n, n_rrq;
   rs_pcg64_state rng;
