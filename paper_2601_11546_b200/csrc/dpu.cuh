@@ -456,7 +456,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       const double* tj = S.small.terms + j * kJobTerms;
       const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
       const int nsm = cnt < kJobTerms ? cnt : kJobTerms;
-#pragma unroll 1
+#pragma unroll 4
       for (int i = 0; i < nsm; ++i) total = __dadd_rn(total, tj[i]);
 #pragma unroll 1
       for (int i = nsm; i < cnt; ++i) total = __dadd_rn(total, spill[i]);  // segments of > 31 sub-batches
