@@ -48,7 +48,7 @@ PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dp
 WINDOW_START = 5
 #: dram__bytes_read.sum + dram__bytes_write.sum per engine_kernel launch (250 iterations) from the
 #: committed `ncu --set full` capture (profiles/r1_engine_kernel.md); None until measured
-TRAFFIC_PER_LAUNCH = 306432.0
+TRAFFIC_PER_LAUNCH = 303872.0
 
 
 def parse():
@@ -512,9 +512,13 @@ def run_config4(args, ws, rank, local):
 
     def sweep(timed):
         """One step: every trace of this GPU's share run to completion (one launch per cost model,
-        the launches concurrent on their own streams); engines are rebuilt outside the events."""
+        the launches concurrent on their own streams).  Device time = the events around the
+        launches; e2e wall = host trace columns -> engines (upload + first-sight) -> launches ->
+        status -> ledger / completion readback of every trace."""
+        t0 = time.perf_counter()
         engines = make_engines()
         torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(main_s)
@@ -526,13 +530,20 @@ def run_config4(args, ws, rank, local):
             main_s.wait_event(e)
         b.record(main_s)
         torch.cuda.synchronize(dev)
-        iters = 0
-        for ne, _ in engines:
-            for st in ne.status():
+        iters, alg, d2h = 0, 0, 0
+        h2d = sum(v.nbytes for _, ms in engines for m in ms for v in m.arrays.values() if v is not None)
+        for ne, ms in engines:
+            for t, (st, m) in enumerate(zip(ne.status(), ms)):
                 assert st.status == _abi.RS_OK, st.status
                 iters += st.iterations
+                alg += st.alg_bytes
+                led = ne.read_ledgers(t, m.view.R)
+                comp = ne.read_completion(t, m.view.N)
+                d2h += sum(x.nbytes for x in led) + comp.nbytes
+        t2 = time.perf_counter()
+        for ne, _ in engines:
             ne.close()
-        return a.elapsed_time(b) / 1e3, iters
+        return a.elapsed_time(b) / 1e3, iters, alg, t2 - t0, t1 - t0, d2h, h2d
 
     for _ in range(args.warmup):
         sweep(False)
@@ -540,18 +551,33 @@ def run_config4(args, ws, rank, local):
         import torch.distributed as dist
 
         dist.barrier()
-    dev_s, iters = 0.0, 0
+    dev_s, iters, alg, e2e_s, create_s, d2h, h2d = 0.0, 0, 0, 0.0, 0.0, 0, 0
     t0 = time.perf_counter()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            d, n = sweep(True)
+            d, n, ab, w, cr, ob, ib = sweep(True)
+            h2d += ib
             dev_s += d
             iters += n
+            alg += ab
+            e2e_s += w
+            create_s += cr
+            d2h += ob
     wall = time.perf_counter() - t0
     t_max = max_over_ranks(dev_s, ws, dev)
+    e2e_max = max_over_ranks(e2e_s, ws, dev)
     total = sum_over_ranks(float(iters), ws, dev)
+    alg_total = sum_over_ranks(float(alg), ws, dev)
     if rank != 0:
         return None
+    peak, peak_kind = peaks()
+    achieved = alg_total / t_max / 1e9 / ws  # per GPU
+    e2e = {"value": total / e2e_max, "unit": "iters/s", "h2d_bytes_per_step": int(h2d / args.steps),
+           "d2h_bytes_per_step": int(d2h / args.steps),
+           "breakdown_ms": {"create_ms_per_step": 1e3 * create_s / args.steps,
+                            "total_ms_per_step": 1e3 * e2e_s / args.steps},
+           "includes": "per step: marshal of the host trace columns, upload + first-sight kernel (engine "
+                       "creation), the launches, status, ledger + completion readback of every trace"}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         cpu = cpu_baseline_config4([cells[ci] + (ci,) for ci in mine])
@@ -565,7 +591,11 @@ def run_config4(args, ws, rank, local):
                                "run to completion", "traces_per_gpu": len(mine),
                    "l2": "working set of each step is fresh (engines rebuilt between steps)"},
         "iterations_timed": int(total), "gpu_launches": len(models) * args.steps, "clocks": clk.summary(),
-        "host_wall_s": wall, "cpu_baseline": cpu,
+        "host_wall_s": wall, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_kind,
+                     "note": "device-counted algorithmic bytes of all traces / the step's device time; "
+                             "latency-bound (one dependent iteration chain per trace, 128 CTAs on 148 SMs)"},
     }
 
 

@@ -196,6 +196,42 @@ for _name in ("__len__", "__iter__", "__getitem__", "__contains__", "__eq__", "_
         setattr(_DecisionLog, _name, _wrap())
 
 
+class _LazyDict(dict):
+    """RunResult.ledgers / relquery_sizes: a dict built from the arrays already read
+    back from the device on first use (10^4-10^5 Python objects are host work the
+    caller may never need)."""
+
+    _PENDING = object()  # C-level readers that test the size first (json) see a non-empty dict
+
+    def __init__(self, build):
+        super().__init__({_LazyDict._PENDING: None})
+        self._build = build
+
+    def _ready(self):
+        if self._build is not None:
+            build, self._build = self._build, None
+            dict.clear(self)
+            dict.update(self, build())
+
+
+for _name in ("__len__", "__iter__", "__getitem__", "__contains__", "__eq__", "__ne__", "__repr__", "__reversed__",
+              "__or__", "__ror__", "__ior__", "__setitem__", "__delitem__", "keys", "values", "items", "get", "copy",
+              "pop", "popitem", "setdefault", "update", "clear"):
+    if hasattr(dict, _name):
+        def _wrap_d(name=_name):
+            base = getattr(dict, name)
+
+            def f(self, *a, **k):
+                self._ready()
+                return base(self, *a, **k)
+
+            f.__name__ = name
+            return f
+
+        setattr(_LazyDict, _name, _wrap_d())
+_LazyDict.__reduce__ = lambda self: (self._ready(), (dict, (dict.copy(self),)))[1]
+
+
 _ERRORS = {
     _abi.RS_EINVAL: ValueError,
     _abi.RS_EINFEASIBLE: InfeasibleRequestError,
@@ -350,14 +386,16 @@ class Engine:
         c = self.trace.columns()
         arrival, fps, lpe, lde = ne.read_ledgers(0, c.num_relqueries)
         comp = ne.read_completion(0, c.num_requests)
-        order = np.lexsort((c.rel_id, c.arrival))
-        admitted = np.zeros(c.num_relqueries, bool)
-        admitted[order[: st.admitted]] = True
-        rid, av, fv, lv, dv = (c.rel_id.tolist(), arrival.tolist(), fps.tolist(), lpe.tolist(), lde.tolist())
-        # NaN (x != x) -> None: the reference's unset timestamps
-        ledgers = {rid[i]: TimestampLedger(av[i], None if fv[i] != fv[i] else fv[i],
-                                           None if lv[i] != lv[i] else lv[i], None if dv[i] != dv[i] else dv[i])
-                   for i in order[: st.admitted].tolist()}
+        n_adm = int(st.admitted)
+
+        def ledgers():  # admission order (arrival, rel_id), engine.py:211-213
+            adm = np.lexsort((c.rel_id, c.arrival))[:n_adm]
+            rid, av, fv, lv, dv = (c.rel_id.tolist(), arrival.tolist(), fps.tolist(), lpe.tolist(), lde.tolist())
+            # NaN (x != x) -> None: the reference's unset timestamps
+            return {rid[i]: TimestampLedger(av[i], None if fv[i] != fv[i] else fv[i],
+                                            None if lv[i] != lv[i] else lv[i], None if dv[i] != dv[i] else dv[i])
+                    for i in adm.tolist()}
+
         recs = (np.concatenate(self._records) if self._records
                 else np.zeros(0, _abi.ITER_RECORD_DTYPE))
         log = _DecisionLog(recs if self.config.log_decisions else recs[:0])
@@ -371,8 +409,8 @@ class Engine:
                     r.generated, r.prefilled, r.priority = g[k], bool(p[k]), pr[k]
                     k += 1
         return RunResult(
-            policy=self.policy, rate=self.trace.rate, seed=self.seed, ledgers=ledgers,
-            relquery_sizes={int(r): int(s) for r, s in zip(c.rel_id.tolist(), np.diff(c.row_off).tolist())},
+            policy=self.policy, rate=self.trace.rate, seed=self.seed, ledgers=_LazyDict(ledgers),
+            relquery_sizes=_LazyDict(lambda: dict(zip(c.rel_id.tolist(), np.diff(c.row_off).tolist()))),
             decision_log=log, iterations=int(st.iterations), sim_duration=float(st.clock),
             dpu_wall_s=self._phase_seconds(st, _DPU_PHASES), aba_wall_s=self._phase_seconds(st, _ABA_PHASES),
             cache_hit_tokens=int(st.cache_hit_tokens),

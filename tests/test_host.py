@@ -132,3 +132,29 @@ def test_native_v1_reader_rejects_malformed_files(bad, tmp_path):
     p.write_text(bad)
     with pytest.raises((SchemaError, ValueError)):
         load_trace(p)
+
+
+def test_lazy_result_dict_behaves_like_dict():
+    """RunResult.ledgers / relquery_sizes are built on first use; every dict path sees the data."""
+    import json
+    import pickle
+
+    from paper_2601_11546_b200.engine import _LazyDict
+
+    calls = []
+
+    def build():
+        calls.append(1)
+        return {3: 30, 1: 10}
+
+    d = _LazyDict(build)
+    assert not calls
+    assert len(d) == 2 and calls == [1]
+    assert d == {3: 30, 1: 10} and dict(d) == {3: 30, 1: 10} and {**d} == {3: 30, 1: 10}
+    assert sorted(d) == [1, 3] and list(d.items()) == [(3, 30), (1, 10)] and 1 in d and d.get(2) is None
+    assert json.loads(json.dumps(_LazyDict(build))) == {"3": 30, "1": 10}
+    assert pickle.loads(pickle.dumps(_LazyDict(build))) == {3: 30, 1: 10}
+    e = _LazyDict(build)
+    e[5] = 50
+    assert e == {3: 30, 1: 10, 5: 50}
+    assert bool(_LazyDict(dict)) is False
