@@ -214,6 +214,14 @@ int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* fir
 int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t* prefilled,
                             int64_t* completion_iter, double* priority);
 
+/*
+ * Completion iteration per request (trace order, -1 = not finished) as int32:
+ * the device column copied straight into `completion_iter` (page-locked
+ * memory makes it one DMA).  The per-request output the reference's ledgers
+ * are derived from (engine.py:358-362); the bulk result of a run.
+ */
+int rs_engine_read_completion(rs_engine* e, int32_t t, int32_t* completion_iter);
+
 /* ---------------------------------------------------------------------------
  * Sharded pool (BASELINE config 5): one trace whose relQueries are
  * owned round-robin by admission rank across `shards` shards.  Each shard

@@ -49,6 +49,8 @@ def lib():
     L.rs_engine_read_ledgers.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
     L.rs_engine_read_requests.restype = C.c_int
     L.rs_engine_read_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
+    L.rs_engine_read_completion.restype = C.c_int
+    L.rs_engine_read_completion.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
     L.rs_engine_destroy.restype = None
     L.rs_engine_destroy.argtypes = [C.c_void_p]
     L.rs_engine_device_bytes.restype = C.c_int64
@@ -100,7 +102,7 @@ def lib():
 #: every symbol include/relserve.h declares
 EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_build_info", "rs_engine_create", "rs_engine_step", "rs_engine_status",
-    "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_destroy",
+    "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_read_completion", "rs_engine_destroy",
     "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
     "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange",
@@ -229,8 +231,12 @@ class NativeEngine:
         return gen, pre, comp, prio
 
     def read_completion(self, t: int, N: int) -> np.ndarray:
-        comp = np.zeros(N, np.int64)
-        _check(lib().rs_engine_read_requests(self.h, t, None, None, comp.ctypes.data, None))
+        """int32 completion iterations, trace order, in page-locked memory from torch's caching
+        host allocator (one DMA; the block returns to the cache when the array is dropped)."""
+        import torch
+
+        comp = torch.empty(N, dtype=torch.int32, pin_memory=True).numpy()
+        _check(lib().rs_engine_read_completion(self.h, t, comp.ctypes.data))
         return comp
 
     def device_bytes(self) -> int:

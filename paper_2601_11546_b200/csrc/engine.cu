@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/relserve.h"
@@ -940,7 +941,7 @@ int arena_reserve(HostTrace& h, size_t bytes) {
 }
 
 template <typename T>
-int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_byte = -1) {
+int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_byte = -1, bool async = false) {
   if (n == 0) n = 1;
   void* q = nullptr;
   const size_t nb = (n * sizeof(T) + 255) & ~(size_t)255;
@@ -955,7 +956,8 @@ int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_by
   h.bytes += (long long)(n * sizeof(T));
   cudaError_t e = cudaSuccess;
   if (src) {
-    e = cudaMemcpy(q, src, n * sizeof(T), cudaMemcpyHostToDevice);
+    e = async ? cudaMemcpyAsync(q, src, n * sizeof(T), cudaMemcpyHostToDevice, 0)
+              : cudaMemcpy(q, src, n * sizeof(T), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   } else if (fill_byte >= 0) {
     e = cudaMemset(q, fill_byte, n * sizeof(T));
@@ -978,6 +980,7 @@ struct rs_engine {
   std::vector<HostTrace> traces;
   TraceDev* d_traces = nullptr;
   size_t smem = 0;
+  cudaEvent_t done = nullptr;  // recorded after every launch: destroy waits on it before the stream-ordered frees
 };
 
 extern "C" {
@@ -1039,9 +1042,8 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   if (!ident) h.row_src.resize(N);
   int max_size = 1;
   long long max_nb = 0, max_tok_all = 0;
-  long long k = 0;
   off[0] = 0;
-  for (long long a = 0; a < R; ++a) {
+  for (long long a = 0; a < R; ++a) {  // per-relQuery columns in admission order (O(R))
     const int t = h.order[a];
     arrival[a] = v.arrival[t];
     ol[a] = v.output_limit[t];
@@ -1054,61 +1056,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     if (hi - lo > max_size) max_size = (int)(hi - lo);
     if (dpu && cfg->sample_size > 200 && hi - lo > 10000)
       return fail(RS_EUNSUPPORTED, "Generator.choice tail-shuffle branch is not replayed");
-    // rows: bulk copy, then range checks on per-relQuery min / max (the
-    // per-row scan below runs only to name the offending row)
-    const long long n = hi - lo;
-    if (n > 0) {
-      if (!ident) {
-        memcpy(&tok[k], v.tok + lo, n * sizeof(int));
-        memcpy(&out[k], v.out + lo, n * sizeof(int));
-        std::iota(h.row_src.begin() + k, h.row_src.begin() + k + n, lo);
-      }
-      int tmin = tok[k], tmax = tok[k], omin = out[k], omax = out[k];
-      for (long long i = k; i < k + n; ++i) {
-        tmin = std::min(tmin, tok[i]);
-        tmax = std::max(tmax, tok[i]);
-        omin = std::min(omin, out[i]);
-        omax = std::max(omax, out[i]);
-      }
-      const long long lim_lo = (long long)chain[a] * cfg->block_size;  // nb >= chain  <=>  tok >= chain * B
-      if (tmin <= 0 || omin < 1 || omax > ol[a] || (long long)tmax + ol[a] > cfg->cap ||
-          (long long)tmax + ol[a] >= (1LL << 20) || tmin < lim_lo) {
-        for (long long r = lo; r < hi; ++r) {
-          const long long tk = v.tok[r], ou = v.out[r];
-          if (tk <= 0) return fail(RS_EINVAL, "request tokens must be non-empty");
-          if (ou < 1 || ou > ol[a]) return fail(RS_EINVAL, "actual_output_len out of range");
-          if (tk + ol[a] > cfg->cap) {
-            char msg[200];
-            snprintf(msg, sizeof msg, "request %lld/%lld needs %lld KV tokens > cap %lld", (long long)relid[a],
-                     (long long)(r - lo), tk + ol[a], (long long)cfg->cap);
-            return fail(RS_EINFEASIBLE, msg);
-          }
-          if (tk + ol[a] >= (1LL << 20))
-            return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
-          if (tk < lim_lo) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
-        }
-      }
-      const long long nb = tmax / cfg->block_size;
-      if (nb > max_nb) max_nb = nb;
-      if (tmax > max_tok_all) max_tok_all = tmax;
-      k += n;
-    }
-    off[a + 1] = (int)k;
-  }
-  if (max_nb > cfg->capacity_blocks)
-    return fail(RS_EUNSUPPORTED, "a request has more whole blocks than the cache capacity (truncated insert)");
-  TraceDev& d = h.dev;
-  d.R = (int)R;
-  d.N = (int)N;
-  d.max_size = max_size;
-  {
-    const long long max_tok = max_tok_all;
-    d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
-    // engine_kernel<true> (no general DPU path) needs count-only PEM segments,
-    // mns and sample size within the warp fast path, and every relQuery's
-    // segments within the job buffers
-    d.fast = d.seg_ok && cfg->max_num_seqs <= kSmallMns && cfg->sample_size <= 16 &&
-             (long long)max_size + cfg->max_num_seqs <= (long long)(kMaxJobs - 1) * cfg->max_num_seqs;
+    off[a + 1] = off[a] + (int)(hi - lo);
   }
   int rc;
 #define TRY(x) \
@@ -1126,12 +1074,110 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
                         rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
                         (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
                         32 * 256;
-    pc.mark("host rows");
     TRY(arena_reserve(h, need));
   }
+  // admission order == trace order: the caller's rows go up now (stream 0, asynchronous
+  // from page-locked memory) while the host threads below validate them
+  struct Drain {
+    bool on = false;
+    ~Drain() {
+      if (on) cudaStreamSynchronize(0);  // the caller's buffers outlive the copy on every return path
+    }
+  } drain;
+  TraceDev& d = h.dev;
+  if (ident) {
+    drain.on = true;
+    TRY(dalloc(h, (int**)&d.tok, N, tok, -1, true));
+    TRY(dalloc(h, (int**)&d.out, N, out, -1, true));
+  }
+  // rows (O(N), the bulk of creation at 10^6-10^7 rows): gather into admission
+  // order unless it is the trace order, and per-relQuery min / max of tok and
+  // out, on host threads over contiguous row ranges
+  std::vector<int> st(4 * R);  // tmin, tmax, omin, omax
+  auto scan_rows = [&](long long a0, long long a1) {
+    for (long long a = a0; a < a1; ++a) {
+      const long long k = off[a], n = off[a + 1] - off[a];
+      if (n == 0) continue;
+      if (!ident) {
+        const long long lo = v.row_off[h.order[a]];
+        memcpy(&tok[k], v.tok + lo, n * sizeof(int));
+        memcpy(&out[k], v.out + lo, n * sizeof(int));
+        std::iota(h.row_src.begin() + k, h.row_src.begin() + k + n, lo);
+      }
+      int tmin = tok[k], tmax = tok[k], omin = out[k], omax = out[k];
+      for (long long i = k; i < k + n; ++i) {
+        tmin = std::min(tmin, tok[i]);
+        tmax = std::max(tmax, tok[i]);
+        omin = std::min(omin, out[i]);
+        omax = std::max(omax, out[i]);
+      }
+      st[4 * a] = tmin, st[4 * a + 1] = tmax, st[4 * a + 2] = omin, st[4 * a + 3] = omax;
+    }
+  };
+  {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nth = (int)std::max<long long>(1, std::min<long long>({N >> 17, 16, hw ? (long long)hw : 1}));
+    std::vector<std::thread> pool;
+    long long a0 = 0;
+    for (int w = 0; w < nth; ++w) {  // split by rows: thread w takes relQueries up to row N*(w+1)/nth
+      const long long row_end = N * (w + 1) / nth;
+      long long a1 = a0;
+      while (a1 < R && (w == nth - 1 || off[a1] < row_end)) ++a1;
+      if (w == nth - 1) a1 = R;
+      if (a1 > a0) {
+        if (w == nth - 1) scan_rows(a0, a1);
+        else pool.emplace_back(scan_rows, a0, a1);
+      }
+      a0 = a1;
+    }
+    for (auto& th : pool) th.join();
+  }
+  for (long long a = 0; a < R; ++a) {  // checks (engine.py:235-239), in admission order
+    if (off[a + 1] == off[a]) continue;
+    const int tmin = st[4 * a], tmax = st[4 * a + 1], omin = st[4 * a + 2], omax = st[4 * a + 3];
+    const long long lim_lo = (long long)chain[a] * cfg->block_size;  // nb >= chain  <=>  tok >= chain * B
+    if (tmin <= 0 || omin < 1 || omax > ol[a] || (long long)tmax + ol[a] > cfg->cap ||
+        (long long)tmax + ol[a] >= (1LL << 20) || tmin < lim_lo) {
+      const long long lo = v.row_off[h.order[a]], hi = v.row_off[h.order[a] + 1];
+      for (long long r = lo; r < hi; ++r) {  // name the offending row
+        const long long tk = v.tok[r], ou = v.out[r];
+        if (tk <= 0) return fail(RS_EINVAL, "request tokens must be non-empty");
+        if (ou < 1 || ou > ol[a]) return fail(RS_EINVAL, "actual_output_len out of range");
+        if (tk + ol[a] > cfg->cap) {
+          char msg[200];
+          snprintf(msg, sizeof msg, "request %lld/%lld needs %lld KV tokens > cap %lld", (long long)relid[a],
+                   (long long)(r - lo), tk + ol[a], (long long)cfg->cap);
+          return fail(RS_EINFEASIBLE, msg);
+        }
+        if (tk + ol[a] >= (1LL << 20))
+          return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
+        if (tk < lim_lo) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
+      }
+    }
+    const long long nb = tmax / cfg->block_size;
+    if (nb > max_nb) max_nb = nb;
+    if (tmax > max_tok_all) max_tok_all = tmax;
+  }
+  if (max_nb > cfg->capacity_blocks)
+    return fail(RS_EUNSUPPORTED, "a request has more whole blocks than the cache capacity (truncated insert)");
+  pc.mark("host rows");
+  d.R = (int)R;
+  d.N = (int)N;
+  d.max_size = max_size;
+  {
+    const long long max_tok = max_tok_all;
+    d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
+    // engine_kernel<true> (no general DPU path) needs count-only PEM segments,
+    // mns and sample size within the warp fast path, and every relQuery's
+    // segments within the job buffers
+    d.fast = d.seg_ok && cfg->max_num_seqs <= kSmallMns && cfg->sample_size <= 16 &&
+             (long long)max_size + cfg->max_num_seqs <= (long long)(kMaxJobs - 1) * cfg->max_num_seqs;
+  }
+  if (!ident) {
+    TRY(dalloc(h, (int**)&d.tok, N, tok));
+    TRY(dalloc(h, (int**)&d.out, N, out));
+  }
   pc.mark("host rows + arena");
-  TRY(dalloc(h, (int**)&d.tok, N, tok));
-  TRY(dalloc(h, (int**)&d.out, N, out));
   std::vector<double> nanv(R, NAN);
   TRY(dalloc(h, &d.fps, R, nanv.data()));
   TRY(dalloc(h, &d.lpe, R, nanv.data()));
@@ -1173,7 +1219,12 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     // rank of each rel_id among all rel_ids: the Delta projection's sort key
     std::vector<int> byid(R);
     std::iota(byid.begin(), byid.end(), 0);
-    std::stable_sort(byid.begin(), byid.end(), [&](int x, int y) { return relid[x] < relid[y]; });
+    if (!std::is_sorted(relid.begin(), relid.end())) {  // (rel_id, rank) pairs: a stable order
+      std::vector<std::pair<long long, int>> kv(R);
+      for (long long a = 0; a < R; ++a) kv[a] = {relid[a], (int)a};
+      std::sort(kv.begin(), kv.end());
+      for (long long i = 0; i < R; ++i) byid[i] = kv[i].second;
+    }
     h.rq_host.assign(rq_bytes((int)R) + 16, 0);
     RqView hv = rq_carve(h.rq_host.data(), (int)R);
     for (long long a = 0; a < R; ++a) {
@@ -1196,14 +1247,15 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
         cudaError_t ce = cudaMemcpy(zp.data(), d.fsprio, R * sizeof(double), cudaMemcpyDeviceToHost);
         if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("first-sight readback: ") + cudaGetErrorString(ce));
       }
-      std::vector<int> z(R);
-      std::iota(z.begin(), z.end(), 0);
-      auto bits = [&](int a) {
+      std::vector<std::pair<unsigned long long, int>> zk(R);  // (priority bits, rank): stable by the rank
+      for (long long a = 0; a < R; ++a) {
         unsigned long long b;
         memcpy(&b, &zp[a], 8);
-        return b;
-      };
-      std::stable_sort(z.begin(), z.end(), [&](int x, int y) { return bits(x) < bits(y); });
+        zk[a] = {b, (int)a};
+      }
+      std::sort(zk.begin(), zk.end());
+      std::vector<int> z(R);
+      for (long long i = 0; i < R; ++i) z[i] = zk[i].second;
       h.zorder = z;
       int nz = 0;  // a shard orders only the relQueries it owns (shard.cuh)
       for (long long i = 0; i < R; ++i)
@@ -1305,7 +1357,7 @@ static int upload_traces(rs_engine* e) {
   const int n = (int)e->traces.size();
   std::vector<TraceDev> devs(n);
   for (int t = 0; t < n; ++t) devs[t] = e->traces[t].dev;
-  if (!e->d_traces && cudaMalloc(&e->d_traces, sizeof(TraceDev) * n) != cudaSuccess)
+  if (!e->d_traces && cudaMallocAsync(&e->d_traces, sizeof(TraceDev) * n, 0) != cudaSuccess)
     return fail(RS_ECUDA, "trace table allocation failed");
   if (cudaMemcpy(e->d_traces, devs.data(), sizeof(TraceDev) * n, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(RS_ECUDA, "trace table upload failed");
@@ -1495,6 +1547,8 @@ int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
   else
     engine_kernel<false><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
   RS_CUDA(cudaGetLastError());
+  if (!e->done) RS_CUDA(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming));
+  RS_CUDA(cudaEventRecord(e->done, (cudaStream_t)stream));
   return RS_OK;
 }
 
@@ -1627,9 +1681,29 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
   return RS_OK;
 }
 
+int rs_engine_read_completion(rs_engine* e, int32_t t, int32_t* completion_iter) {
+  if (!e || t < 0 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
+  const HostTrace& h = e->traces[t];
+  const int N = h.dev.N;
+  RS_CUDA(cudaSetDevice(e->device));
+  if (!N) return RS_OK;
+  if (h.row_src.empty()) {  // admission order == trace order
+    RS_CUDA(cudaMemcpy(completion_iter, h.dev.comp, (size_t)N * 4, cudaMemcpyDeviceToHost));
+    return RS_OK;
+  }
+  std::vector<int> comp(N);
+  RS_CUDA(cudaMemcpy(comp.data(), h.dev.comp, (size_t)N * 4, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < N; ++k) completion_iter[h.row_src[k]] = comp[k];
+  return RS_OK;
+}
+
 void rs_engine_destroy(rs_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
+  if (e->done) {  // the last launch may still run on a non-blocking stream
+    cudaEventSynchronize(e->done);
+    cudaEventDestroy(e->done);
+  }
   if (e->mbox) cudaFree(e->mbox);
   if (e->d_peers) cudaFree(e->d_peers);
   for (auto& h : e->traces) {
@@ -1637,7 +1711,7 @@ void rs_engine_destroy(rs_engine* e) {
     if (h.arena_alloc) cudaFreeAsync(h.arena_alloc, 0);
     if (h.noise_buf) cudaFree(h.noise_buf);
   }
-  if (e->d_traces) cudaFree(e->d_traces);
+  if (e->d_traces) cudaFreeAsync(e->d_traces, 0);
   delete e;
 }
 

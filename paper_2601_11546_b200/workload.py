@@ -230,6 +230,24 @@ class ArrivalTrace:
             self._columns = _columns_from_entries(self._entries)
         return self._columns
 
+    def pin_memory(self) -> "ArrivalTrace":
+        """Move the column arrays into page-locked host memory (torch's pinned host
+        allocator), so engine creation uploads them by DMA instead of through the
+        driver's pageable staging.  Returns self; values are unchanged."""
+        import dataclasses
+
+        import torch
+
+        c = self.columns()
+
+        def pin(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+        self._columns = dataclasses.replace(
+            c, **{f: pin(getattr(c, f)) for f in ("rel_id", "arrival", "output_limit", "prefix_len", "row_off",
+                                                   "tok", "out")})
+        return self
+
     def _columns_stale(self) -> bool:
         c = self._columns
         if c.num_relqueries != len(self._entries):
