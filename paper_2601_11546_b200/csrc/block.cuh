@@ -39,6 +39,21 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
   return v;
 }
 
+// 32-bit: the shuffle's own in-range predicate guards the add (two
+// instructions per step, no lane compares) -- the scans are the largest
+// block of hot code in the scheduler iteration.
+template <>
+__device__ __forceinline__ int warp_incl_scan<int>(int v) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1)
+    asm("{\n\t.reg .b32 o;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 o|p, %0, %1, 0, -1;\n\t"
+        "@p add.s32 %0, %0, o;\n\t}"
+        : "+r"(v)
+        : "r"(d));
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
