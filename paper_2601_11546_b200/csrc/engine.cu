@@ -36,6 +36,10 @@
 #include <vector>
 
 #include "../../include/relserve.h"
+
+#ifndef RS_PREFETCH_HEAD
+#define RS_PREFETCH_HEAD 1  // the previous head's next candidate rows, prefetched into L1 during the DPU
+#endif
 #include "cache_model.cuh"
 #include "dpu.cuh"
 #include "engine_state.cuh"
@@ -224,6 +228,19 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   __syncthreads();
   if (!S.go_admit) return false;
   phase_mark(c, 0);
+#if RS_PREFETCH_HEAD
+  if (tid >= kThreads - 32) {  // the last warp: pull the previous head's next candidate rows into L1
+    const int h = S.head, l = tid & 31;
+    if (h >= 0 && l < 18) {
+      const int lo = rq.off[h] + rq.q[h], hi = rq.off[h + 1];
+      const int r = lo + (l % 9) * 32;  // 9 lines of 128 B cover the <= 256 rows of a candidate
+      if (r < hi) {
+        const int* p = (l < 9 ? T.tok : T.out) + r;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+      }
+    }
+  }
+#endif
 
   // ---- B: priorities.  fcfs: 0.0; sp: static_relquery_prio, both set at
   // admission (engine.py:255-267, preloaded into prio); relserve*: the DPU.
@@ -705,7 +722,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   const size_t rqb = rq_bytes(T.R);
   void* rq_base = T.rq_in_smem ? (void*)(smem_raw + ((sizeof(Shared) + 15) & ~(size_t)15)) : T.rq_global;
   if (T.rq_in_smem) copy16(rq_base, T.rq_global, rqb);
-  if (threadIdx.x == 0) S.rq = rq_carve(rq_base, T.R);
+  if (threadIdx.x == 0) {
+    S.rq = rq_carve(rq_base, T.R);
+    S.head = -1;  // no previous head to prefetch for
+  }
   __syncthreads();
   if (S.c.status == RS_RUNNING) {
     if (threadIdx.x == 0) S.c.phase[kPhases - 1] = clock64();
