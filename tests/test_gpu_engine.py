@@ -133,3 +133,29 @@ def test_device_full_waiting_order_matches_reference(name):
             assert got == e["order"], f"{name}: waiting order differs at iteration {e['it']}"
             n += 1
     assert n > 0
+
+
+def test_pinned_trace_and_result_readback():
+    """Page-locked trace columns (the e2e path) give the identical run; the int32
+    completion readback equals read_requests' completion column; the lazily built
+    ledgers / sizes equal an eager build."""
+    from paper_2601_11546_b200 import EngineConfig, TraceConfig, generate_trace, world_preset
+    from paper_2601_11546_b200.engine import Engine
+
+    tc = TraceConfig(num_relqueries=60, size_range=(1, 90), rate=6.0, seed=17)
+    w = world_preset("opt-13b-like")
+    a, _ = run_device(generate_trace(tc), "relserve", w, EngineConfig(), None, 3)
+    pinned = generate_trace(tc).pin_memory()
+    assert all(getattr(pinned.columns(), f).flags["C_CONTIGUOUS"] for f in ("tok", "out", "row_off"))
+    eng = Engine(pinned, "relserve", w, EngineConfig(), None, 3, device=0)
+    b = eng.run()
+    _, _, comp64, _ = eng.requests_state
+    eng.close()
+    assert b.completion_iteration.dtype == np.int32
+    assert np.array_equal(b.completion_iteration, comp64)
+    assert np.array_equal(a.completion_iteration, b.completion_iteration)
+    for k in a.records.dtype.names:
+        assert np.array_equal(a.records[k], b.records[k], equal_nan=a.records[k].dtype.kind == "f"), k
+    assert dict(a.ledgers) == dict(b.ledgers) and len(b.ledgers) == 60
+    c = pinned.columns()
+    assert dict(b.relquery_sizes) == {int(r): int(s) for r, s in zip(c.rel_id, np.diff(c.row_off))}
