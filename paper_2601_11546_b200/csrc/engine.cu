@@ -230,7 +230,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   phase_mark(c, 0);
 #if RS_PREFETCH_HEAD
   if (tid >= kThreads - 32) {  // the last warp: pull the previous head's next candidate rows into L1
-    const int h = S.head, l = tid & 31;
+    const int h = S.pf_head, l = tid & 31;
     if (h >= 0 && l < 18) {
       const int lo = rq.off[h] + rq.q[h], hi = rq.off[h + 1];
       const int r = lo + (l % 9) * 32;  // 9 lines of 128 B cover the <= 256 rows of a candidate
@@ -695,6 +695,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       c.n_log++;
     }
     c.iteration++;
+    S.pf_head = S.head;  // read after the next admission barrier
   }
   phase_mark(c, 4);
   // no closing barrier: the next admission (thread 0) touches nothing the other threads
@@ -724,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   if (T.rq_in_smem) copy16(rq_base, T.rq_global, rqb);
   if (threadIdx.x == 0) {
     S.rq = rq_carve(rq_base, T.R);
-    S.head = -1;  // no previous head to prefetch for
+    S.pf_head = -1;  // no previous head to prefetch for
   }
   __syncthreads();
   if (S.c.status == RS_RUNNING) {

@@ -191,6 +191,7 @@ struct Shared {
   int go_admit;  // phase A's continue flag (separate from `go`: no barrier closes an iteration)
   int new_lo, new_hi;
   int head, W, taken, J;
+  int pf_head;  // the previous iteration's head (candidate-row prefetch), set at the iteration end
   long long utok_sum;
   double m_plus, m_minus;
   int dmin_slot, n_est;
