@@ -261,8 +261,19 @@ __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7FF8000
 #define RS_PHASE_TIMERS 1
 #endif
 __device__ __forceinline__ void phase_mark(Ctl& c, int k) {
-#if RS_PHASE_TIMERS
-  if (RS_PHASE_TIMERS >= 2 || k < 5) {
+#if RS_PHASE_TIMERS >= 2
+  // the clock read waits for a shared-memory load, which cannot complete before
+  // a preceding barrier does (a bare read may retire under BAR.SYNC.DEFER_BLOCKING
+  // and charge the barrier wait to the next phase)
+  if (threadIdx.x == 0) {
+    const long long prev = *(volatile long long*)&c.phase[kPhases - 1];
+    long long now = prev;
+    if (prev != 0x7FFFFFFFFFFFFFFFLL) now = clock64();
+    c.phase[k] += now - prev;
+    c.phase[kPhases - 1] = now;
+  }
+#elif RS_PHASE_TIMERS
+  if (k < 5) {  // coarse phases only (each may absorb the tail of the preceding barrier wait)
     if (threadIdx.x == 0) {
       const long long now = clock64();
       c.phase[k] += now - c.phase[kPhases - 1];
