@@ -880,6 +880,39 @@ __global__ void __launch_bounds__(kThreads) first_sight_kernel(int R, const int*
   }
 }
 
+// Engine-creation row checks (engine.py:235-239 and the device model's limits),
+// one warp per relQuery over the uploaded rows: res[0] = the first admission
+// rank with an offending row (INT_MAX if none), res[1] = the largest tok.  The
+// host names the offending row only when res[0] says there is one.
+__global__ void __launch_bounds__(kThreads) validate_rows_kernel(int R, const int* off, const int* ol, const int* chain,
+                                                                 const int* tok, const int* out, long long B,
+                                                                 long long cap, int* res) {
+  const int warps = gridDim.x * kWarps, lane = threadIdx.x & 31;
+  for (int a = blockIdx.x * kWarps + (threadIdx.x >> 5); a < R; a += warps) {
+    const int lo = off[a], hi = off[a + 1];
+    if (hi == lo) continue;
+    int tmin = 0x7FFFFFFF, tmax = -0x7FFFFFFF - 1, omin = 0x7FFFFFFF, omax = -0x7FFFFFFF - 1;
+    for (int i = lo + lane; i < hi; i += 32) {
+      const int t = tok[i], o = out[i];
+      tmin = t < tmin ? t : tmin;
+      tmax = t > tmax ? t : tmax;
+      omin = o < omin ? o : omin;
+      omax = o > omax ? o : omax;
+    }
+    tmin = __reduce_min_sync(kFull, tmin);
+    tmax = __reduce_max_sync(kFull, tmax);
+    omin = __reduce_min_sync(kFull, omin);
+    omax = __reduce_max_sync(kFull, omax);
+    if (lane == 0) {
+      const long long o = ol[a];
+      if (tmin <= 0 || omin < 1 || omax > o || tmax + o > cap || tmax + o >= (1LL << 20) ||
+          tmin < (long long)chain[a] * B)
+        atomicMin(&res[0], a);
+      atomicMax(&res[1], tmax);
+    }
+  }
+}
+
 }  // namespace rsd
 
 // ===========================================================================
@@ -1094,7 +1127,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
                         8 * (size_t)(R + 1) + 8 * (size_t)R + 8 * (size_t)(R + 1) + 4 * (size_t)R +
                         rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
                         (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
-                        32 * 256;
+                        12 * (size_t)(R + 1) + 8 + 36 * 256;
     TRY(arena_reserve(h, need));
   }
   // admission order == trace order: the caller's rows go up now (stream 0, asynchronous
@@ -1114,7 +1147,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   // rows (O(N), the bulk of creation at 10^6-10^7 rows): gather into admission
   // order unless it is the trace order, and per-relQuery min / max of tok and
   // out, on host threads over contiguous row ranges
-  std::vector<int> st(4 * R);  // tmin, tmax, omin, omax
+  std::vector<int> st;  // tmin, tmax, omin, omax per relQuery
   auto scan_rows = [&](long long a0, long long a1) {
     for (long long a = a0; a < a1; ++a) {
       const long long k = off[a], n = off[a + 1] - off[a];
@@ -1135,7 +1168,8 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       st[4 * a] = tmin, st[4 * a + 1] = tmax, st[4 * a + 2] = omin, st[4 * a + 3] = omax;
     }
   };
-  {
+  auto host_scan = [&]() {
+    st.assign(4 * R, 0);
     const unsigned hw = std::thread::hardware_concurrency();
     const int nth = (int)std::max<long long>(1, std::min<long long>({N >> 17, 16, hw ? (long long)hw : 1}));
     std::vector<std::thread> pool;
@@ -1152,57 +1186,71 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       a0 = a1;
     }
     for (auto& th : pool) th.join();
-  }
-  for (long long a = 0; a < R; ++a) {  // checks (engine.py:235-239), in admission order
-    if (off[a + 1] == off[a]) continue;
-    const int tmin = st[4 * a], tmax = st[4 * a + 1], omin = st[4 * a + 2], omax = st[4 * a + 3];
-    const long long lim_lo = (long long)chain[a] * cfg->block_size;  // nb >= chain  <=>  tok >= chain * B
-    if (tmin <= 0 || omin < 1 || omax > ol[a] || (long long)tmax + ol[a] > cfg->cap ||
-        (long long)tmax + ol[a] >= (1LL << 20) || tmin < lim_lo) {
-      const long long lo = v.row_off[h.order[a]], hi = v.row_off[h.order[a] + 1];
-      for (long long r = lo; r < hi; ++r) {  // name the offending row
-        const long long tk = v.tok[r], ou = v.out[r];
-        if (tk <= 0) return fail(RS_EINVAL, "request tokens must be non-empty");
-        if (ou < 1 || ou > ol[a]) return fail(RS_EINVAL, "actual_output_len out of range");
-        if (tk + ol[a] > cfg->cap) {
-          char msg[200];
-          snprintf(msg, sizeof msg, "request %lld/%lld needs %lld KV tokens > cap %lld", (long long)relid[a],
-                   (long long)(r - lo), tk + ol[a], (long long)cfg->cap);
-          return fail(RS_EINFEASIBLE, msg);
+  };
+  auto check_rows = [&]() -> int {
+    for (long long a = 0; a < R; ++a) {  // checks (engine.py:235-239), in admission order
+      if (off[a + 1] == off[a]) continue;
+      const int tmin = st[4 * a], tmax = st[4 * a + 1], omin = st[4 * a + 2], omax = st[4 * a + 3];
+      const long long lim_lo = (long long)chain[a] * cfg->block_size;  // nb >= chain  <=>  tok >= chain * B
+      if (tmin <= 0 || omin < 1 || omax > ol[a] || (long long)tmax + ol[a] > cfg->cap ||
+          (long long)tmax + ol[a] >= (1LL << 20) || tmin < lim_lo) {
+        const long long lo = v.row_off[h.order[a]], hi = v.row_off[h.order[a] + 1];
+        for (long long r = lo; r < hi; ++r) {  // name the offending row
+          const long long tk = v.tok[r], ou = v.out[r];
+          if (tk <= 0) return fail(RS_EINVAL, "request tokens must be non-empty");
+          if (ou < 1 || ou > ol[a]) return fail(RS_EINVAL, "actual_output_len out of range");
+          if (tk + ol[a] > cfg->cap) {
+            char msg[200];
+            snprintf(msg, sizeof msg, "request %lld/%lld needs %lld KV tokens > cap %lld", (long long)relid[a],
+                     (long long)(r - lo), tk + ol[a], (long long)cfg->cap);
+            return fail(RS_EINFEASIBLE, msg);
+          }
+          if (tk + ol[a] >= (1LL << 20))
+            return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
+          if (tk < lim_lo) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
         }
-        if (tk + ol[a] >= (1LL << 20))
-          return fail(RS_EUNSUPPORTED, "tok + output_limit must be below 2^20 (32-bit device prefix sums)");
-        if (tk < lim_lo) return fail(RS_EUNSUPPORTED, "chain_blocks exceeds a row's whole blocks");
       }
+      const long long nb = tmax / cfg->block_size;
+      if (nb > max_nb) max_nb = nb;
+      if (tmax > max_tok_all) max_tok_all = tmax;
     }
-    const long long nb = tmax / cfg->block_size;
-    if (nb > max_nb) max_nb = nb;
-    if (tmax > max_tok_all) max_tok_all = tmax;
+    return RS_OK;
+  };
+  // admission order == trace order: the rows are checked on the device, where they
+  // are being uploaded (read back after the first-sight kernel); otherwise on the
+  // host threads that gather them
+  int *d_off = nullptr, *d_ol = nullptr, *d_res = nullptr;
+  if (ident) {
+    int* d_chain = nullptr;
+    const int init[2] = {0x7FFFFFFF, 0};
+    TRY(dalloc(h, &d_off, R + 1, off.data()));
+    TRY(dalloc(h, &d_ol, R, ol.data()));
+    TRY(dalloc(h, &d_chain, R, chain.data()));
+    TRY(dalloc(h, &d_res, 2, init));
+    if (R > 0) {
+      const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
+      validate_rows_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d_chain, d.tok, d.out, cfg->block_size, cfg->cap,
+                                               d_res);
+      const cudaError_t ke = cudaGetLastError();
+      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("validate_rows_kernel: ") + cudaGetErrorString(ke));
+    }
+  } else {
+    host_scan();
+    TRY(check_rows());
   }
-  if (max_nb > cfg->capacity_blocks)
-    return fail(RS_EUNSUPPORTED, "a request has more whole blocks than the cache capacity (truncated insert)");
   pc.mark("host rows");
   d.R = (int)R;
   d.N = (int)N;
   d.max_size = max_size;
-  {
-    const long long max_tok = max_tok_all;
-    d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
-    // engine_kernel<true> (no general DPU path) needs count-only PEM segments,
-    // mns and sample size within the warp fast path, and every relQuery's
-    // segments within the job buffers
-    d.fast = d.seg_ok && cfg->max_num_seqs <= kSmallMns && cfg->sample_size <= 16 &&
-             (long long)max_size + cfg->max_num_seqs <= (long long)(kMaxJobs - 1) * cfg->max_num_seqs;
-  }
   if (!ident) {
     TRY(dalloc(h, (int**)&d.tok, N, tok));
     TRY(dalloc(h, (int**)&d.out, N, out));
   }
   pc.mark("host rows + arena");
-  std::vector<double> nanv(R, NAN);
-  TRY(dalloc(h, &d.fps, R, nanv.data()));
-  TRY(dalloc(h, &d.lpe, R, nanv.data()));
-  TRY(dalloc(h, &d.lde, R, nanv.data()));
+  // unset ledger timestamps: all-ones bytes are a NaN (the host maps any NaN to None)
+  TRY(dalloc(h, &d.fps, R, nullptr, 0xFF));
+  TRY(dalloc(h, &d.lpe, R, nullptr, 0xFF));
+  TRY(dalloc(h, &d.lde, R, nullptr, 0xFF));
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
   TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
@@ -1220,11 +1268,32 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     for (long long a = 0; a < R; ++a) fsd[a + 1] = fsd[a] + ((off[a + 1] - off[a]) > cfg->sample_size ? dper : 0);
     TRY(dalloc(h, (long long**)&d.fs_doff, R + 1, fsd.data()));
     TRY(dalloc(h, (double**)&d.fsprio, R, nullptr, 0));
+    if (ident) {  // the device row checks (before any kernel reads the rows)
+      int res[2];
+      const cudaError_t ce = cudaMemcpy(res, d_res, sizeof res, cudaMemcpyDeviceToHost);
+      if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("row check readback: ") + cudaGetErrorString(ce));
+      if (res[0] != 0x7FFFFFFF) {  // name the offending row (the host checks stop at it)
+        host_scan();
+        TRY(check_rows());
+        return fail(RS_ECUDA, "device row check disagrees with the host");
+      }
+      max_tok_all = res[1];
+      max_nb = max_tok_all / cfg->block_size;
+    }
+    if (max_nb > cfg->capacity_blocks)
+      return fail(RS_EUNSUPPORTED, "a request has more whole blocks than the cache capacity (truncated insert)");
+    {
+      const long long max_tok = max_tok_all;
+      d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
+      // engine_kernel<true> (no general DPU path) needs count-only PEM segments,
+      // mns and sample size within the warp fast path, and every relQuery's
+      // segments within the job buffers
+      d.fast = d.seg_ok && cfg->max_num_seqs <= kSmallMns && cfg->sample_size <= 16 &&
+               (long long)max_size + cfg->max_num_seqs <= (long long)(kMaxJobs - 1) * cfg->max_num_seqs;
+    }
     if (R > 0 && cfg->policy >= RS_POLICY_RELSERVE) {
-      int* d_off = nullptr;
-      int* d_ol = nullptr;
-      TRY(dalloc(h, &d_off, R + 1, off.data()));
-      TRY(dalloc(h, &d_ol, R, ol.data()));
+      if (!d_off) TRY(dalloc(h, &d_off, R + 1, off.data()));
+      if (!d_ol) TRY(dalloc(h, &d_ol, R, ol.data()));
       PemModel m{h.pol.alpha_p, h.pol.beta_p, h.pol.alpha_d, h.pol.beta_d, cfg->cap, cfg->max_num_seqs,
                  cfg->max_num_batched_tokens};
       const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
@@ -1345,10 +1414,10 @@ static int clone_replica(const HostTrace& src, const rs_config* cfg, const rs_pc
                       16 + (size_t)d.fifo_cap * sizeof(FifoEnt) + (size_t)d.log_cap * sizeof(rs_iter_record) +
                       sizeof(Ctl) + 16 * 256;
   TRY(arena_reserve(h, need));
-  std::vector<double> nanv(R, NAN);
-  TRY(dalloc(h, &d.fps, R, nanv.data()));
-  TRY(dalloc(h, &d.lpe, R, nanv.data()));
-  TRY(dalloc(h, &d.lde, R, nanv.data()));
+  // unset ledger timestamps: all-ones bytes are a NaN (the host maps any NaN to None)
+  TRY(dalloc(h, &d.fps, R, nullptr, 0xFF));
+  TRY(dalloc(h, &d.lpe, R, nullptr, 0xFF));
+  TRY(dalloc(h, &d.lde, R, nullptr, 0xFF));
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
   TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
@@ -1360,7 +1429,12 @@ static int clone_replica(const HostTrace& src, const rs_config* cfg, const rs_pc
     d.nzl = nz;
     d.shard_world = shard_world;
     d.shard_rank = shard_rank;
-    TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
+    // the table is shard 0's (device to device) but for this shard's static order
+    TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size()));
+    const size_t zl_at = (size_t)((const unsigned char*)hv.zl - h.rq_host.data());
+    if (cudaMemcpyAsync(d.rq_global, src.dev.rq_global, h.rq_host.size(), cudaMemcpyDeviceToDevice, 0) != cudaSuccess ||
+        cudaMemcpy((unsigned char*)d.rq_global + zl_at, hv.zl, (size_t)R * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(RS_ECUDA, "replica relQuery table copy failed");
   }
   TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
   if (d.log_cap > 0) TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
