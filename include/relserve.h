@@ -301,6 +301,19 @@ int rs_pem_batch(int64_t n_sets, const int64_t* item_off, const int64_t* utok,
                  const rs_cost_model* model, double* values_out, int32_t device);
 
 /*
+ * Unit entry point of the waiting order (engine.py:277-281 sort key
+ * (priority, arrival, rel_id), of which the engine needs only the head and
+ * len(waiting)): over n relQueries given in admission order -- sorted by
+ * (arrival, rel_id), engine.py:211-213 -- the first minimum of `priority`
+ * among those with waiting[i] != 0 (*head = -1 if none) and their count.  The
+ * engine's own full-scan reduction on the device.  Priorities of waiting
+ * entries must be non-negative (every policy's are); EINVAL otherwise.
+ * Replaces: the `waiting.sort(key=...)` + `waiting[0]` pair of Engine.run.
+ */
+int rs_waiting_argmin(const double* priority, const uint8_t* waiting, int64_t n, int32_t device, int64_t* head,
+                      int64_t* count);
+
+/*
  * The Adaptive Batch Arranger for given candidates (the engine's device code):
  * project_delta(prefill, output_limit_p, running, W, model) (arranger.py:115-143)
  * when both candidates are non-empty and m_plus <= m_minus, then decide_next

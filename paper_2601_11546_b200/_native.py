@@ -49,6 +49,8 @@ def lib():
     L.rs_engine_read_ledgers.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
     L.rs_engine_read_requests.restype = C.c_int
     L.rs_engine_read_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
+    L.rs_waiting_argmin.restype = C.c_int
+    L.rs_waiting_argmin.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
     L.rs_engine_read_completion.restype = C.c_int
     L.rs_engine_read_completion.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
     L.rs_engine_destroy.restype = None
@@ -102,10 +104,10 @@ def lib():
 #: every symbol include/relserve.h declares
 EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_build_info", "rs_engine_create", "rs_engine_step", "rs_engine_status",
-    "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_read_completion", "rs_engine_destroy",
-    "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
+    "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_read_completion",
+    "rs_engine_destroy", "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
-    "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange",
+    "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange", "rs_waiting_argmin",
     "rs_engine_read_order", "rs_trace_v1_load", "rs_trace_v1_info", "rs_trace_v1_columns", "rs_trace_v1_free",
     "rs_trace_v1_error",
 )
@@ -294,6 +296,19 @@ def arrange(running, d_min_rel_id, prefill_n, prefill_utok, prefill_rel_id, pref
                             nan if m_minus is None else float(m_minus), int(n_waiting), _abi.POLICY_IDS[policy],
                             C.byref(cm), device, out.ctypes.data))
     return out[0]
+
+
+def waiting_argmin(priority, waiting, device=0):
+    """The device waiting-queue head (include/relserve.h rs_waiting_argmin): entries in admission
+    order; returns (head index or -1, number waiting)."""
+    p = np.ascontiguousarray(priority, np.float64)
+    w = np.ascontiguousarray(waiting, np.uint8)
+    if p.shape != w.shape:
+        raise ValueError("priority and waiting differ in length")
+    head, count = C.c_int64(), C.c_int64()
+    _check(lib().rs_waiting_argmin(p.ctypes.data if len(p) else None, w.ctypes.data if len(w) else None, len(p),
+                                   device, C.byref(head), C.byref(count)))
+    return head.value, count.value
 
 
 def read_trace_v1(path):

@@ -913,6 +913,32 @@ __global__ void __launch_bounds__(kThreads) validate_rows_kernel(int R, const in
   }
 }
 
+// Unit entry point of the waiting order (rs_waiting_argmin): the engine's
+// full-scan head reduction -- ranks visited in increasing order with a strict
+// `<`, then block_count_argmin -- over given priorities and waiting flags.
+__global__ void __launch_bounds__(kThreads) waiting_argmin_kernel(long long n, const double* prio,
+                                                                  const unsigned char* waiting, long long* out) {
+  __shared__ RedSmem red;
+  int w = 0;
+  unsigned long long key = ~0ULL;
+  int idx = 0x7FFFFFFF;
+  for (long long a = threadIdx.x; a < n; a += kThreads) {
+    if (waiting[a]) {
+      ++w;
+      const unsigned long long k = dbits(prio[a]);
+      if (k < key) {
+        key = k;
+        idx = (int)a;
+      }
+    }
+  }
+  block_count_argmin(w, key, idx, red);
+  if (threadIdx.x == 0) {
+    out[0] = idx == 0x7FFFFFFF ? -1 : idx;
+    out[1] = w;
+  }
+}
+
 }  // namespace rsd
 
 // ===========================================================================
@@ -1900,6 +1926,36 @@ int rs_arrange(int32_t n_run, const int64_t* run_rel_id, const int64_t* run_outp
   RS_CUDA(cudaMemcpy(out, d_out, sizeof(rs_iter_record), cudaMemcpyDeviceToHost));
   cudaFree(d);
   cudaFree(d_out);
+  return RS_OK;
+}
+
+int rs_waiting_argmin(const double* priority, const uint8_t* waiting, int64_t n, int32_t device, int64_t* head,
+                      int64_t* count) {
+  if (n < 0 || n > 0x7FFFFFF0LL || (n && (!priority || !waiting)) || !head || !count)
+    return fail(RS_EINVAL, "bad waiting-order input");
+  for (long long a = 0; a < n; ++a)  // the bit order equals the value order for these only
+    if (waiting[a] && !(priority[a] >= 0.0)) return fail(RS_EINVAL, "priorities must be non-negative numbers");
+  RS_CUDA(cudaSetDevice(device));
+  double* d_p = nullptr;
+  unsigned char* d_w = nullptr;
+  long long* d_out = nullptr;
+  const size_t m = (size_t)std::max<long long>(n, 1);
+  RS_CUDA(cudaMalloc(&d_p, m * sizeof(double)));
+  RS_CUDA(cudaMalloc(&d_w, m));
+  RS_CUDA(cudaMalloc(&d_out, 2 * sizeof(long long)));
+  if (n) {
+    RS_CUDA(cudaMemcpy(d_p, priority, n * sizeof(double), cudaMemcpyHostToDevice));
+    RS_CUDA(cudaMemcpy(d_w, waiting, n, cudaMemcpyHostToDevice));
+  }
+  waiting_argmin_kernel<<<1, kThreads>>>(n, d_p, d_w, d_out);
+  RS_CUDA(cudaGetLastError());
+  long long res[2];
+  RS_CUDA(cudaMemcpy(res, d_out, sizeof res, cudaMemcpyDeviceToHost));
+  cudaFree(d_p);
+  cudaFree(d_w);
+  cudaFree(d_out);
+  *head = res[0];
+  *count = res[1];
   return RS_OK;
 }
 

@@ -51,3 +51,24 @@ def test_choice_sequence_matches_numpy():
     want = np.concatenate([g.choice(int(n), size=int(k), replace=False) for n, k in zip(ns, ks)])
     assert got.tolist() == want.tolist()
     assert st.to_numpy()["state"] == g.bit_generator.state["state"]
+
+
+def test_waiting_argmin_matches_reference_sort():
+    """rs_waiting_argmin == waiting.sort(key=(priority, arrival, rel_id))[0] and len(waiting)
+    (engine.py:277-281, 161-176) on entries in admission order, ties included."""
+    from paper_2601_11546_b200._native import waiting_argmin
+
+    r = np.random.default_rng(5)
+    for n in (0, 1, 7, 512, 513, 5000, 70_000):
+        prio = r.choice([0.0, 0.25, 1.5, 3.0], n) if n % 2 else r.uniform(0, 10, n)
+        wait = r.random(n) < 0.6
+        head, count = waiting_argmin(prio, wait)
+        ranks = np.flatnonzero(wait)
+        assert count == len(ranks)
+        if not len(ranks):
+            assert head == -1
+            continue
+        # admission order is (arrival, rel_id), so rank order breaks priority ties
+        assert head == ranks[np.lexsort((ranks, prio[ranks]))[0]]
+    with pytest.raises(ValueError):
+        waiting_argmin(np.array([1.0, -2.0]), np.array([1, 1]))
