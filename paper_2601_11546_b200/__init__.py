@@ -30,11 +30,13 @@ from .priority import (
     PriorityRecord,
     RemainderItem,
     SchedulerConstraints,
+    pem,
     pem_batch,
     remainder_items,
     static_relquery_prio,
     static_req_prio,
 )
+from .report import decompose
 from .workload import (
     OUTPUT_LIMITS,
     ArrivalTrace,
@@ -50,11 +52,11 @@ from .workload import (
 )
 
 __all__ = [
-    "ArrivalTrace", "DecisionLogEntry", "Engine", "EngineConfig", "InfeasibleRequestError",
+    "ArrivalTrace", "DecisionLogEntry", "decompose", "Engine", "EngineConfig", "InfeasibleRequestError",
     "LinearCostModel", "OUTPUT_LIMITS", "POLICIES", "PriorityRecord", "QueryType", "RelQuery",
     "RemainderItem", "Request", "RunResult", "SchedulerConstraints", "SimulationAborted",
     "TimestampLedger", "TraceColumns", "TraceConfig", "WORLD_PRESETS", "generate_heavy_tail_trace",
-    "generate_trace", "load_model", "load_trace", "pem_batch", "predict_decode", "predict_prefill",
+    "generate_trace", "load_model", "load_trace", "pem", "pem_batch", "predict_decode", "predict_prefill",
     "remainder_items", "run", "save_model", "save_trace", "static_relquery_prio", "static_req_prio",
     "world_preset",
 ]

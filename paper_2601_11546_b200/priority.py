@@ -99,3 +99,11 @@ def pem_batch(remainders: Sequence[Sequence[RemainderItem]] | Sequence[tuple],
     cat = (lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt))
     return _native.pem_batch(np.asarray(offs, np.int64), cat(utok, np.int64), cat(rem, np.int32),
                              cat(pre, np.uint8), constraints, model, device)
+
+
+def pem(items: Sequence[RemainderItem], constraints: SchedulerConstraints, model: LinearCostModel,
+        device: int = 0) -> float:
+    """relsim's `pem(items, constraints, model)` (priority.py:163-218): the estimated
+    remaining duration of one remainder, by the engine's device PEM (rs_pem_batch)."""
+    return float(pem_batch([items], constraints, model, device)[0])
+

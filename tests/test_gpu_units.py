@@ -72,3 +72,19 @@ def test_waiting_argmin_matches_reference_sort():
         assert head == ranks[np.lexsort((ranks, prio[ranks]))[0]]
     with pytest.raises(ValueError):
         waiting_argmin(np.array([1.0, -2.0]), np.array([1, 1]))
+
+
+def test_pem_reference_tests():
+    """pkg/tests/test_priority.py TestPem (:180-200) through the drop-in `pem`."""
+    from paper_2601_11546_b200 import RemainderItem, pem
+
+    model = LinearCostModel(0.001, 0.02, 0.0002, 0.015)
+    c = SchedulerConstraints(cap=1000, max_num_seqs=10, max_num_batched_tokens=500)
+    items = [RemainderItem(None, u, 2, False) for u in (100, 60, 40)]
+    assert pem(items, c, model) == pytest.approx(0.22 + 2 * 0.0156)
+    assert pem([], c, model) == 0.0
+    lo = pem([RemainderItem(None, 50, 3, False)] * 4, c, model)
+    hi = pem([RemainderItem(None, 100, 3, False)] * 4, c, model)
+    assert hi >= lo
+    full = pem([RemainderItem(None, 80, 4, False)] * 6, c, model)
+    assert pem([RemainderItem(None, 80, 4, False)] * 5, c, model) <= full
