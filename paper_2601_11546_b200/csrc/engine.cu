@@ -78,7 +78,9 @@ __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_fir
     return;
   }
   double ddp = 0, ddm = 0, ddt = 0;
-  if (has_p && has_d && m_plus <= m_minus) {  // project_delta
+  // project_delta: the reference also evaluates it for internal decisions
+  // (engine.py:397-415), but only the transitional case reads it (arranger.py:146-179)
+  if (has_p && has_d && !internal && m_plus <= m_minus) {
     const double l_prefill = __dadd_rn(__dmul_rn(m.alpha_p, (double)utok_sum), m.beta_p);
     ddp = __dmul_rn(l_prefill, (double)n_dist);
     long long max_ol = 0;
@@ -461,7 +463,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
 
   // ---- E: decision (engine.py:387-433, arranger.py:115-179)
   const bool has_p = S.taken > 0, has_d = c.n_run > 0;
-  const bool need_proj = !P.prefill_first && has_p && has_d && S.m_plus <= S.m_minus;
+  const bool need_proj = !P.prefill_first && has_p && has_d && S.dmin_slot != S.head && S.m_plus <= S.m_minus;
   if (need_proj) {
     // distinct running relQueries sorted by rel_id (engine.py:406-408)
     const int nd = c.n_rrq;
