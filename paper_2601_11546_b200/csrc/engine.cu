@@ -1244,11 +1244,12 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     }
     return RS_OK;
   };
-  // admission order == trace order: the rows are checked on the device, where they
-  // are being uploaded (read back after the first-sight kernel); otherwise on the
-  // host threads that gather them
+  // admission order == trace order and many rows: the rows are checked on the
+  // device, where they are being uploaded (read back before the first kernel
+  // that reads them); otherwise on the host (threads that also gather them)
+  const bool dev_check = ident && N >= (1LL << 16);
   int *d_off = nullptr, *d_ol = nullptr, *d_res = nullptr;
-  if (ident) {
+  if (dev_check) {
     int* d_chain = nullptr;
     const int init[2] = {0x7FFFFFFF, 0};
     TRY(dalloc(h, &d_off, R + 1, off.data()));
@@ -1296,7 +1297,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     for (long long a = 0; a < R; ++a) fsd[a + 1] = fsd[a] + ((off[a + 1] - off[a]) > cfg->sample_size ? dper : 0);
     TRY(dalloc(h, (long long**)&d.fs_doff, R + 1, fsd.data()));
     TRY(dalloc(h, (double**)&d.fsprio, R, nullptr, 0));
-    if (ident) {  // the device row checks (before any kernel reads the rows)
+    if (dev_check) {  // the device row checks (before any kernel reads the rows)
       int res[2];
       const cudaError_t ce = cudaMemcpy(res, d_res, sizeof res, cudaMemcpyDeviceToHost);
       if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("row check readback: ") + cudaGetErrorString(ce));

@@ -161,33 +161,40 @@ def test_pinned_trace_and_result_readback():
     assert dict(b.relquery_sizes) == {int(r): int(s) for r, s in zip(c.rel_id, np.diff(c.row_off))}
 
 
+@pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("ident", [True, False])
-def test_creation_row_checks(ident):
+def test_creation_row_checks(ident, big):
     """engine.py:235-239 and the device model's row limits, checked on the device
-    (admission order == trace order) or on the host (otherwise): same exception,
-    same message naming the offending request."""
+    (admission order == trace order, >= 2^16 rows) or on the host (otherwise): same
+    exception, same message naming the offending request."""
     from paper_2601_11546_b200 import EngineConfig, SchedulerConstraints, world_preset
     from paper_2601_11546_b200.engine import Engine
     from paper_2601_11546_b200.priority import InfeasibleRequestError
     from paper_2601_11546_b200.workload import ArrivalTrace, TraceColumns
 
-    def trace(tok, out):
+    n0, n1 = (40_000, 40_000) if big else (2, 3)
+
+    def trace(bad_tok=None, bad_out=None):
+        tok = np.full(n0 + n1, 100, np.int32)
+        out = np.full(n0 + n1, 5, np.int32)
+        if bad_tok is not None:
+            tok[n0 + 1] = bad_tok
+        if bad_out is not None:
+            out[n0 + 1] = bad_out
         ids = [3, 7] if ident else [7, 3]  # equal arrivals: admission order is by rel_id
         return ArrivalTrace(columns=TraceColumns(
             rel_id=np.array(ids, np.int64), arrival=np.zeros(2), output_limit=np.array([10, 10], np.int32),
-            prefix_len=np.zeros(2, np.int32), row_off=np.array([0, 2, 5], np.int64),
-            tok=np.array(tok, np.int32), out=np.array(out, np.int32), token_seed=0))
+            prefix_len=np.zeros(2, np.int32), row_off=np.array([0, n0, n0 + n1], np.int64),
+            tok=tok, out=out, token_seed=0))
 
     w = world_preset("opt-13b-like")
-    cfg = EngineConfig(constraints=SchedulerConstraints(cap=500, max_num_seqs=16, max_num_batched_tokens=400))
-    ok_tok, ok_out = [100, 120, 90, 80, 70], [5, 10, 1, 2, 3]
-    eng = Engine(trace(ok_tok, ok_out), "relserve", w, cfg, None, 0, device=0)
-    assert eng.run().iterations > 0
-    eng.close()
+    cfg = EngineConfig(constraints=SchedulerConstraints(cap=500, max_num_seqs=16, max_num_batched_tokens=400),
+                       iteration_limit=50)
+    Engine(trace(), "relserve", w, cfg, None, 0, device=0).close()
     with pytest.raises(ValueError, match="non-empty"):
-        Engine(trace([100, 120, 90, 0, 70], ok_out), "relserve", w, cfg, None, 0, device=0)
+        Engine(trace(bad_tok=0), "relserve", w, cfg, None, 0, device=0)
     with pytest.raises(ValueError, match="out of range"):
-        Engine(trace(ok_tok, [5, 10, 11, 2, 3]), "relserve", w, cfg, None, 0, device=0)
-    rid = 7 if ident else 3  # trace row 3 is row 1 of the second relQuery in trace order
+        Engine(trace(bad_out=11), "relserve", w, cfg, None, 0, device=0)
+    rid = 7 if ident else 3  # the second relQuery in trace order
     with pytest.raises(InfeasibleRequestError, match=rf"request {rid}/1 needs 501 KV tokens > cap 500"):
-        Engine(trace([100, 120, 90, 491, 70], ok_out), "relserve", w, cfg, None, 0, device=0)
+        Engine(trace(bad_tok=491), "relserve", w, cfg, None, 0, device=0)
