@@ -1,0 +1,101 @@
+"""Full runs at BASELINE's full sizes (configs 2 and 3: 10^6 requests; config 5:
+8*10^6 requests sharded 8 ways), checked through size-independent properties --
+the CPU oracle needs minutes per thousand iterations here, so the bit-exact
+comparisons stay on the golden windows (test_gpu_engine.py) and these runs check
+what must hold of any correct run to completion:
+
+* every request is prefilled once and decoded to its EOS point: the prefill
+  batches of a relQuery cover its rows exactly once, decode batches add up to
+  sum(out) row-iterations, every request has a completion iteration;
+* token conservation: cache hit + miss tokens == sum(tok) (test_engine.py:197-206);
+* batch invariants: kv_reserved <= cap and back to 0, batch sizes <= mns
+  (test_engine.py:181-195); the clock never decreases and ends at the last decode;
+* ledgers: arrival <= first prefill <= last prefill <= last decode, and the latency
+  breakdown sums exactly (test_engine.py:78-88);
+* config 5: the 8-shard run equals the unsharded run record for record.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _trace(config):
+    from paper_2601_11546_b200 import (EngineConfig, TraceConfig, generate_heavy_tail_trace, generate_trace,
+                                       world_preset)
+
+    if config == 2:
+        t = generate_trace(TraceConfig(num_relqueries=1000, size_range=(1000, 1000), rate=1e6, seed=0))
+        return t, world_preset("opt-13b-like"), EngineConfig()
+    n = 5000 if config == 3 else 40_000
+    t = generate_heavy_tail_trace(num_relqueries=n, size_range=(1, 399), rate=1e6, seed=0)
+    return t, world_preset("llama-70b-like"), EngineConfig()
+
+
+def _run(trace, world, cfg, shards=1):
+    from paper_2601_11546_b200.engine import Engine
+
+    eng = Engine(trace, "relserve", world, cfg, None, 0, device=0, shards=shards)
+    eng.chunk_iterations = 1 << 16
+    try:
+        res = eng.run()
+    finally:
+        eng.close()
+    return res
+
+
+def _check_run(res, trace, cfg):
+    from paper_2601_11546_b200.report import decompose
+
+    c = trace.columns()
+    recs = res.records
+    cons = cfg.constraints
+    assert len(recs) == res.iterations
+    assert np.array_equal(recs["iteration"], np.arange(res.iterations))
+    # every request prefilled exactly once, relQuery by relQuery, in row order
+    pre = recs[recs["action"] == 0]
+    sizes = np.diff(c.row_off)
+    order = np.lexsort((c.rel_id, c.arrival))  # admission rank -> trace index
+    covered = np.zeros(len(sizes), np.int64)
+    np.add.at(covered, order[pre["batch_rq"]], pre["batch_n"])
+    assert np.array_equal(covered, sizes)
+    # decode batches: one token per running row per decode = sum of EOS points
+    dec = recs[recs["action"] == 1]
+    assert int(dec["batch_n"].astype(np.int64).sum()) == int(c.out.astype(np.int64).sum())
+    assert (res.completion_iteration >= 0).all()
+    assert int(res.completion_iteration.max()) == res.iterations - 1
+    # conservation and batch invariants
+    assert res.cache_hit_tokens + res.cache_miss_tokens == int(c.tok.astype(np.int64).sum())
+    assert (recs["kv_reserved"] <= cons.cap).all() and recs["kv_reserved"][-1] == 0
+    assert (recs["batch_n"] <= cons.max_num_seqs).all()
+    assert (pre["batch_n"] >= 1).all()
+    assert (np.diff(recs["clock"]) >= 0).all()
+    # ledgers
+    assert len(res.ledgers) == len(sizes)
+    last = 0.0
+    for rel_id, led in res.ledgers.items():
+        assert led.complete
+        assert led.arrival <= led.first_prefill_start <= led.last_prefill_end <= led.last_decode_end
+        b = decompose(rel_id, led)
+        assert b.waiting_s + b.core_s + b.tail_s == b.total_s
+        last = max(last, led.last_decode_end)
+    assert res.sim_duration == last
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_full_run_properties(config):
+    trace, world, cfg = _trace(config)
+    _check_run(_run(trace, world, cfg), trace, cfg)
+
+
+def test_config5_sharded_full_run_equals_unsharded():
+    trace, world, cfg = _trace(5)
+    a = _run(trace, world, cfg, shards=1)
+    b = _run(trace, world, cfg, shards=8)
+    assert (a.iterations, a.sim_duration) == (b.iterations, b.sim_duration)
+    for k in a.records.dtype.names:
+        assert np.array_equal(a.records[k], b.records[k], equal_nan=a.records[k].dtype.kind == "f"), k
+    assert np.array_equal(a.completion_iteration, b.completion_iteration)
+    assert (a.cache_hit_tokens, a.cache_miss_tokens) == (b.cache_hit_tokens, b.cache_miss_tokens)
+    _check_run(b, trace, cfg)
