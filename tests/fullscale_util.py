@@ -1,0 +1,45 @@
+"""Workloads and run fingerprints shared by tests/test_gpu_fullscale.py and
+tests/golden/make_fullscale.py (BASELINE configs 2 and 3 at full size)."""
+
+import hashlib
+
+import numpy as np
+
+_NAN = np.int64(0x7FF8000000000000)
+
+
+def _config2():
+    from paper_2601_11546_b200 import EngineConfig, TraceConfig, generate_trace, world_preset
+
+    t = generate_trace(TraceConfig(num_relqueries=1000, size_range=(1000, 1000), rate=1e6, seed=0))
+    return t, world_preset("opt-13b-like"), EngineConfig()
+
+
+def _config3():
+    from paper_2601_11546_b200 import EngineConfig, generate_heavy_tail_trace, world_preset
+
+    t = generate_heavy_tail_trace(num_relqueries=5000, size_range=(1, 399), rate=1e6, seed=0)
+    return t, world_preset("llama-70b-like"), EngineConfig()
+
+
+WORKLOADS = {"config2": _config2, "config3": _config3}
+
+#: decision-record fields compared (rs_iter_record; the oracle's log has the same names)
+FIELDS = ("iteration", "clock", "m_plus", "m_minus", "delta_plus", "delta_minus", "delta_total", "kv_reserved",
+          "action", "kase", "head", "n_waiting", "batch_rq", "batch_first", "batch_n", "n_reestimated")
+
+
+def _canon(a: np.ndarray) -> bytes:
+    a = np.asarray(a)
+    if a.dtype.kind == "f":
+        b = a.astype("<f8").view("<i8").copy()
+        b[np.isnan(a)] = _NAN
+        return b.tobytes()
+    return a.astype("<i8").tobytes()
+
+
+def fingerprint(records: np.ndarray, completion: np.ndarray) -> dict:
+    fp = {f"sha256_{k}": hashlib.sha256(_canon(records[k])).hexdigest() for k in FIELDS}
+    fp["sha256_completion"] = hashlib.sha256(_canon(completion)).hexdigest()
+    fp["records"] = int(len(records))
+    return fp
