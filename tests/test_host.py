@@ -158,3 +158,26 @@ def test_lazy_result_dict_behaves_like_dict():
     e[5] = 50
     assert e == {3: 30, 1: 10, 5: 50}
     assert bool(_LazyDict(dict)) is False
+
+
+def test_fullscale_fingerprint_canonical():
+    """The full-run fingerprints (tests/fullscale_util.py) ignore NaN payloads and
+    integer widths, and the committed oracle fingerprints cover configs 2 and 3."""
+    import json
+    from pathlib import Path
+
+    from fullscale_util import FIELDS, fingerprint
+
+    from paper_2601_11546_b200 import _abi
+
+    r1 = np.zeros(3, _abi.ITER_RECORD_DTYPE)
+    r1["m_plus"] = [1.0, np.nan, 2.0]
+    r2 = r1.copy()
+    r2["m_plus"][1] = -np.nan  # another NaN bit pattern
+    assert fingerprint(r1, np.array([1, -1], np.int32)) == fingerprint(r2, np.array([1, -1], np.int64))
+    r2["m_plus"][2] = 2.0000000000000004
+    assert fingerprint(r1, np.zeros(1))["sha256_m_plus"] != fingerprint(r2, np.zeros(1))["sha256_m_plus"]
+    g = json.loads((Path(__file__).parent / "golden" / "fullscale.json").read_text())
+    for name in ("config2", "config3"):
+        assert all(f"sha256_{k}" in g["configs"][name] for k in FIELDS)
+        assert g["configs"][name]["records"] == g["configs"][name]["iterations"] > 100_000
