@@ -12,7 +12,7 @@ size-independent properties -- what must hold of any correct run to completion:
   breakdown sums exactly (test_engine.py:78-88);
 * config 5: the 8-shard run equals the unsharded run record for record.
 
-Configs 2 and 3 are also compared bit for bit with the CPU oracle's complete runs
+Configs 2 and 3 (config 3 under every policy) are also compared bit for bit with the CPU oracle's complete runs
 (about two minutes each on one core; the Python reference would need hours)
 through fingerprints: SHA-256 per decision-record field and of the per-request
 completion iterations, exact final clock and cache counters
@@ -42,10 +42,10 @@ def _trace(config):
     return t, world_preset("llama-70b-like"), EngineConfig()
 
 
-def _run(trace, world, cfg, shards=1):
+def _run(trace, world, cfg, shards=1, policy="relserve"):
     from paper_2601_11546_b200.engine import Engine
 
-    eng = Engine(trace, "relserve", world, cfg, None, 0, device=0, shards=shards)
+    eng = Engine(trace, policy, world, cfg, None, 0, device=0, shards=shards)
     eng.chunk_iterations = 1 << 16
     try:
         res = eng.run()
@@ -92,14 +92,18 @@ def _check_run(res, trace, cfg):
     assert res.sim_duration == last
 
 
-@pytest.mark.parametrize("config", [2, 3])
-def test_full_run_properties_and_oracle_fingerprint(config):
-    from fullscale_util import WORKLOADS, fingerprint
+_GOLDEN = json.loads((Path(__file__).parent / "golden" / "fullscale.json").read_text())["configs"]
 
-    trace, world, cfg = WORKLOADS[f"config{config}"]()
-    res = _run(trace, world, cfg)
+
+@pytest.mark.parametrize("name", sorted(_GOLDEN))
+def test_full_run_properties_and_oracle_fingerprint(name):
+    from fullscale_util import RUNS, WORKLOADS, fingerprint
+
+    wl, policy = RUNS[name]
+    trace, world, cfg = WORKLOADS[wl]()
+    res = _run(trace, world, cfg, policy=policy)
     _check_run(res, trace, cfg)
-    g = json.loads((Path(__file__).parent / "golden" / "fullscale.json").read_text())["configs"][f"config{config}"]
+    g = _GOLDEN[name]
     assert res.iterations == g["iterations"]
     assert repr(float(res.sim_duration)) == g["clock"]
     assert (res.cache_hit_tokens, res.cache_miss_tokens) == (g["cache_hit_tokens"], g["cache_miss_tokens"])
