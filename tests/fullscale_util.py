@@ -27,7 +27,9 @@ WORKLOADS = {"config2": _config2, "config3": _config3}
 #: complete runs fingerprinted: name -> (workload, policy)
 RUNS = {"config2": ("config2", "relserve"), "config3": ("config3", "relserve"),
         "config3_fcfs": ("config3", "fcfs"), "config3_sp": ("config3", "sp"),
-        "config3_pp": ("config3", "relserve-pp"), "config3_dp": ("config3", "relserve-dp")}
+        "config3_pp": ("config3", "relserve-pp"), "config3_dp": ("config3", "relserve-dp"),
+        "config2_fcfs": ("config2", "fcfs"), "config2_sp": ("config2", "sp"),
+        "config2_pp": ("config2", "relserve-pp"), "config2_dp": ("config2", "relserve-dp")}
 
 #: decision-record fields compared (rs_iter_record; the oracle's log has the same names)
 FIELDS = ("iteration", "clock", "m_plus", "m_minus", "delta_plus", "delta_minus", "delta_total", "kv_reserved",

@@ -12,7 +12,7 @@ size-independent properties -- what must hold of any correct run to completion:
   breakdown sums exactly (test_engine.py:78-88);
 * config 5: the 8-shard run equals the unsharded run record for record.
 
-Configs 2 and 3 (config 3 under every policy) are also compared bit for bit with the CPU oracle's complete runs
+Configs 2 and 3 under every policy are also compared bit for bit with the CPU oracle's complete runs
 (about two minutes each on one core; the Python reference would need hours)
 through fingerprints: SHA-256 per decision-record field and of the per-request
 completion iterations, exact final clock and cache counters
