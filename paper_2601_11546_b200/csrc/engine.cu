@@ -1208,8 +1208,15 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       while (a1 < R && (w == nth - 1 || off[a1] < row_end)) ++a1;
       if (w == nth - 1) a1 = R;
       if (a1 > a0) {
-        if (w == nth - 1) scan_rows(a0, a1);
-        else pool.emplace_back(scan_rows, a0, a1);
+        bool spawned = false;
+        if (w < nth - 1) {
+          try {  // no exception may cross the C ABI: a thread that cannot start scans inline
+            pool.emplace_back(scan_rows, a0, a1);
+            spawned = true;
+          } catch (...) {
+          }
+        }
+        if (!spawned) scan_rows(a0, a1);
       }
       a0 = a1;
     }
