@@ -157,6 +157,7 @@ __device__ __noinline__ long long floyd_tok_sum_any(const int* tok, const unsign
 // Processes the estimated relQueries [e0, e0 + n) of this iteration's list
 // (act then arrivals) for the largest n <= min(32, e1 - e0) whose PEM
 // segments fit kMaxJobs; returns n (0 if even one does not fit).
+template <bool kC>
 __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const PemModel& pm, int e0, int e1) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -172,7 +173,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
   if (lane < n_est) {
     const int ge = e0 + lane;
     a = ge < n_act ? c.act[ge] : S.new_lo + (ge - n_act);
-    own = T.shard_world == 1 || a % T.shard_world == T.shard_rank;
+    own = kC || T.shard_world == 1 || a % T.shard_world == T.shard_rank;
     const int off = rq.off[a];
     const int q = rq.q[a];
     base = off + q;
@@ -854,7 +855,7 @@ __device__ void dpu_batched(const Params& P, const TraceDev& T, Shared& S, const
   }
 }
 
-template <bool kFast>
+template <bool kFast, bool kC>
 __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -872,7 +873,7 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
     // partially prefilled relQueries (in rank order), then the arrivals
     const int n_act = c.n_act;
     for (int e0 = 0; e0 < n_act;) {
-      e0 += dpu_small(P, T, S, pm, e0, n_act);
+      e0 += dpu_small<kC>(P, T, S, pm, e0, n_act);
       __syncthreads();
     }
     if (S.new_hi > S.new_lo) first_sight(P, T, S, S.new_lo, S.new_hi);
@@ -881,7 +882,7 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
     dpu_batched(P, T, S, pm);
   }
   // starvation override (priority.py:318-339): wholly waiting = no prefilled row = q == 0
-  if (isfinite(cfg.tau)) {
+  if (!kC && isfinite(cfg.tau)) {
     for (int a = tid; a < c.n_admitted; a += kThreads) {
       const int size = rq.off[a + 1] - rq.off[a];
       if (rq.q[a] == 0 && size > 0) {

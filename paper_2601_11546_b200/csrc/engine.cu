@@ -175,15 +175,19 @@ __device__ __noinline__ void record_waiting_order(const TraceDev& T, Shared& S, 
 
 // _world_duration (engine.py:310-313): base * (1 + sigma * z), clamped at 0,
 // z = the n-th standard normal of the engine's noise stream (one per executed batch)
+template <bool kC>
 __device__ __forceinline__ double world_duration(const Params& P, const TraceDev& T, long long n, double base) {
-  if (P.cfg.noise_sigma > 0) {
+  if (!kC && P.cfg.noise_sigma > 0) {
     const double v = __dmul_rn(base, __dadd_rn(1.0, __dmul_rn(P.cfg.noise_sigma, T.noise[n])));
     base = v > 0.0 ? v : 0.0;  // max(0.0, v)
   }
   return base;
 }
 
-template <bool kFast>
+// kC: the common configuration, fixed at compile time (a DPU policy, tau = inf,
+// no world-model noise, no waiting-order recording, one shard): the checks for
+// everything else leave the iteration's instruction stream.
+template <bool kFast, bool kC>
 __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -199,7 +203,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     } else if (c.iteration >= cfg.iteration_limit) {
       c.status = RS_EABORT_LIMIT;
       S.go_admit = 0;
-    } else if (cfg.noise_sigma > 0 && c.n_batch >= T.noise_n) {
+    } else if (!kC && cfg.noise_sigma > 0 && c.n_batch >= T.noise_n) {
       S.go_admit = 0;  // out of noise draws: end the launch, still running (the host appends more)
     } else {
       // admission ranks are sorted by arrival: gallop, then bisect, to the first arrival > clock
@@ -246,8 +250,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
 
   // ---- B: priorities.  fcfs: 0.0; sp: static_relquery_prio, both set at
   // admission (engine.py:255-267, preloaded into prio); relserve*: the DPU.
-  if (P.use_dpu) {
-    dpu_update<kFast>(P, T, S);
+  if (kC || P.use_dpu) {
+    dpu_update<kFast, kC>(P, T, S);
   } else if (tid == 0) {
     S.n_est = 0;
   }
@@ -271,11 +275,12 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     const int lane = tid & 31;
     unsigned long long key = ~0ULL;
     int idx = 0x7FFFFFFF;
-    bool full = !P.zorder;
-    if (P.zorder && c.zh_valid) {  // the static-order head is unchanged since the last scan
+    const bool zorder = kC || P.zorder, use_dpu = kC || P.use_dpu;
+    bool full = !zorder;
+    if (zorder && c.zh_valid) {  // the static-order head is unchanged since the last scan
       key = c.zh_key;
       idx = c.zh_idx;
-    } else if (P.zorder) {
+    } else if (zorder) {
       int i0 = c.zptr;
       bool lead = true;
       for (int round = 0;; ++round) {
@@ -291,7 +296,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
           a = rq.zl[i];
           const int q = rq.q[a], sz = rq.off[a + 1] - rq.off[a];
           // DPU policies: leaves the static order at its first prefill; sp/fcfs: when fully prefilled
-          gone = P.use_dpu ? (q > 0 || sz == 0) : q >= sz;
+          gone = use_dpu ? (q > 0 || sz == 0) : q >= sz;
           elig = !gone && a < c.n_admitted;
         }
         if (lead) {
@@ -314,13 +319,13 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     zkey = key;  // the static-order head
     zidx = idx;
-    z_cache = P.zorder && !full;
-    if (P.zorder) {
-      if (P.use_dpu) {  // partially prefilled relQueries with pending rows (this shard's)
+    z_cache = zorder && !full;
+    if (zorder) {
+      if (use_dpu) {  // partially prefilled relQueries with pending rows (this shard's)
         bool better = false;  // this lane holds one that beats the static-order head
         for (int j = lane; j < c.n_act; j += 32) {
           const int a = c.act[j];
-          if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
+          if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (kC || T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
             const unsigned long long k = dbits(rq.prio[a]);
             if (k < key || (k == key && a < idx)) {
               key = k;
@@ -363,7 +368,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       }
       block_count_argmin(w, key, idx, S.red);  // result is block-uniform in registers
     }
-    if (T.shard_world > 1) {  // allgather of the shards' heads and priorities
+    if (!kC && T.shard_world > 1) {  // allgather of the shards' heads and priorities
       if (!shard_exchange(T, S, key, idx)) return false;
     }
     head_l = c.n_wait > 0 && idx != 0x7FFFFFFF ? idx : -1;
@@ -376,7 +381,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       S.head = head_l;  // read by other threads only after later barriers
     }
   }
-  if (cfg.record_order && T.order_buf) record_waiting_order(T, S, c.n_log & (T.log_cap - 1));
+  if (!kC && cfg.record_order && T.order_buf) record_waiting_order(T, S, c.n_log & (T.log_cap - 1));
   phase_mark(c, 2);
 
   // ---- D: candidates (engine.py:285-308)
@@ -463,7 +468,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
 
   // ---- E: decision (engine.py:387-433, arranger.py:115-179)
   const bool has_p = S.taken > 0, has_d = c.n_run > 0;
-  const bool need_proj = !P.prefill_first && has_p && has_d && S.dmin_slot != S.head && S.m_plus <= S.m_minus;
+  const bool need_proj = (kC || !P.prefill_first) && has_p && has_d && S.dmin_slot != S.head && S.m_plus <= S.m_minus;
   if (need_proj) {
     // distinct running relQueries sorted by rel_id (engine.py:406-408)
     const int nd = c.n_rrq;
@@ -480,7 +485,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     int action, kase;
     double dp, dm, dt, mp, mmn;
     const int* sd = S.sorted_dist;
-    arrange(P.pol, P.prefill_first, P.force, has_p, has_d, S.dmin_slot == S.head, S.m_plus, S.m_minus, S.utok_sum,
+    arrange(P.pol, !kC && P.prefill_first, P.force, has_p, has_d, S.dmin_slot == S.head, S.m_plus, S.m_minus, S.utok_sum,
             S.taken, need_proj ? rq.ol[S.head] : 0, need_proj ? S.n_dist : 0, [&](int i) { return (long long)rq.ol[sd[i]]; },
             S.W, action, kase, mp, mmn, dp, dm, dt);
     S.action = action;
@@ -542,14 +547,14 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         c.alg_bytes += 16LL * n;  // FIFO pushes (window reads are counted in prefill_fast)
         const double start = c.clock;
         const double dur =
-            world_duration(P, T, c.n_batch++, __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p));
+            world_duration<kC>(P, T, c.n_batch++, __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p));
         c.n_run = n_run0 + n;
         rq.q[h] = q + n;
         if (h == c.zh_idx) c.zh_valid = 0;  // the cached static-order head may have left the order
         if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
         if (rq.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
         rq.nrun[h] += n;
-        if (q == 0 && P.use_dpu) {  // becomes partially prefilled: join the re-estimate list
+        if (q == 0 && (kC || P.use_dpu)) {  // becomes partially prefilled: join the re-estimate list
           int pos = c.n_act;
           if (pos >= kMaxAct) {
             c.status = RS_EUNSUPPORTED;
@@ -596,7 +601,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     }
     __syncthreads();
     const double clk = __dadd_rn(
-        c.clock, world_duration(P, T, c.n_batch, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d)));
+        c.clock, world_duration<kC>(P, T, c.n_batch, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d)));
     int kv_free = 0;
     int keep[kMaxRun / kThreads], nrow[kMaxRun / kThreads], nrank[kMaxRun / kThreads];
     int ngen[kMaxRun / kThreads], nout[kMaxRun / kThreads], nkv[kMaxRun / kThreads];
@@ -664,7 +669,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
           if (rq.nrun[c.rrq[i]] > 0) c.rrq[w++] = c.rrq[i];
         c.n_rrq = w;
       }
-      if (S.act_dirty && P.use_dpu) {  // drop retired relQueries from the re-estimate list
+      if (S.act_dirty && (kC || P.use_dpu)) {  // drop retired relQueries from the re-estimate list
         int w = 0;
         for (int i = 0; i < c.n_act; ++i) {
           const int a = c.act[i];
@@ -711,7 +716,7 @@ __device__ __forceinline__ void copy16(void* dst, const void* src, size_t bytes)
   for (size_t i = threadIdx.x; i < bytes / 16; i += kThreads) d[i] = s[i];
 }
 
-template <bool kFast>
+template <bool kFast, bool kC>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ TraceDev Tsm;  // the trace's pointers, read on every access
@@ -733,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   if (S.c.status == RS_RUNNING) {
     if (threadIdx.x == 0) S.c.phase[kPhases - 1] = clock64();
     for (long long it = 0; it < P.max_iters; ++it)
-      if (!iterate<kFast>(P, T, S)) break;
+      if (!iterate<kFast, kC>(P, T, S)) break;
   }
   __syncthreads();
   // running rows' generated counts back to HBM (finished rows were written at completion)
@@ -1057,7 +1062,8 @@ struct rs_engine {
   ShardRec* mbox = nullptr;              // this engine's mailbox(es)
   ShardRec** d_peers = nullptr;          // device array [world] of peer mailbox pointers
   bool connected = true;                 // one-shard engines: peers' mailboxes known (rs_engine_connect)
-  bool fast = true;  // every trace qualifies for engine_kernel<true>
+  bool fast = true;  // every trace qualifies for engine_kernel<true, *>
+  bool common = false;  // ... and the configuration is the common one (engine_kernel<true, true>)
   Params params{};
   std::vector<HostTrace> traces;
   TraceDev* d_traces = nullptr;
@@ -1573,9 +1579,14 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   e->smem = need;
   e->fast = true;
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;
-  cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  // the common configuration's specialised kernel (see iterate)
+  e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && !cfg->record_order &&
+              shard_world == 1;
+  cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce == cudaSuccess)
-    ce = cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+    ce = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  if (ce == cudaSuccess)
+    ce = cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce != cudaSuccess) return bail(fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
   pc.mark("kernel attributes");
   *out = e;
@@ -1673,10 +1684,12 @@ int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
   if (e->params.cfg.log_decisions && cap > 0 && max_iters > cap) max_iters = cap;
   Params p = e->params;
   p.max_iters = max_iters;
-  if (e->fast)
-    engine_kernel<true><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
+  if (e->common)
+    engine_kernel<true, true><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
+  else if (e->fast)
+    engine_kernel<true, false><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
   else
-    engine_kernel<false><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
+    engine_kernel<false, false><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
   RS_CUDA(cudaGetLastError());
   if (!e->done) RS_CUDA(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming));
   RS_CUDA(cudaEventRecord(e->done, (cudaStream_t)stream));
