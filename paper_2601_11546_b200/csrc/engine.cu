@@ -185,8 +185,8 @@ __device__ __forceinline__ double world_duration(const Params& P, const TraceDev
 }
 
 // kC: the common configuration, fixed at compile time (a DPU policy, tau = inf,
-// no world-model noise, no waiting-order recording, one shard): the checks for
-// everything else leave the iteration's instruction stream.
+// no world-model noise, no waiting-order recording, one shard, decision log on):
+// the checks for everything else leave the iteration's instruction stream.
 template <bool kFast, bool kC>
 __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   Ctl& c = S.c;
@@ -495,7 +495,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       c.zh_idx = zidx;
       c.zh_valid = 1;
     }
-    if (cfg.log_decisions && T.log_cap > 0) {
+    if (kC || (cfg.log_decisions && T.log_cap > 0)) {
       c.alg_bytes += sizeof(rs_iter_record);
       rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
       r.iteration = c.iteration;
@@ -571,7 +571,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         c.clock = __dadd_rn(c.clock, dur);
         if (q == 0) T.fps[h] = start;  // first_prefill_start is set once (engine.py:338-339)
         T.lpe[h] = c.clock;
-        if (cfg.log_decisions && T.log_cap > 0) {
+        if (kC || (cfg.log_decisions && T.log_cap > 0)) {
           rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
           r.batch_rq = h;
           r.batch_first = q;
@@ -662,7 +662,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       c.kv -= kv_total;
       c.clock = clk;
       c.n_batch++;
-      if (cfg.log_decisions && T.log_cap > 0) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
+      if (kC || (cfg.log_decisions && T.log_cap > 0)) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
       if (S.rrq_dirty) {
         int w = 0;
         for (int i = 0; i < c.n_rrq; ++i)
@@ -683,7 +683,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       if (c.n_admitted >= T.R) {
         c.status = c.live ? RS_EABORT_IDLE : RS_OK;
         S.go = 0;
-        if (cfg.log_decisions && T.log_cap > 0) {
+        if (kC || (cfg.log_decisions && T.log_cap > 0)) {
           T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
           c.n_log++;
         }
@@ -697,7 +697,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     if (!S.go) return false;
   }
   if (tid == 0) {
-    if (cfg.log_decisions && T.log_cap > 0) {
+    if (kC || (cfg.log_decisions && T.log_cap > 0)) {
       T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
       c.n_log++;
     }
@@ -1581,7 +1581,8 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;
   // the common configuration's specialised kernel (see iterate)
   e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && !cfg->record_order &&
-              shard_world == 1;
+              shard_world == 1 && cfg->log_decisions;
+  for (auto& h : e->traces) e->common = e->common && h.dev.log_cap > 0;
   cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce == cudaSuccess)
     ce = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
