@@ -201,12 +201,13 @@ __device__ void drain_sequential(Shared& S, const TraceDev& T, long long E, int 
 // in shared memory) and the chain candidates.  Returns false (nothing
 // changed) when the preconditions fail; the caller then runs the exact
 // per-row path.  tokv: the batch rows' tok (staged by the candidate scan).
+template <bool kC>
 __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int h, int n, const int* tokv,
                              long long& ut_out) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const int tid = threadIdx.x;
-  const long long B = P.cfg.block_size;
+  const long long B = kC ? 16 : P.cfg.block_size;  // kC: the default block size (engine.py:152)
   const long long C = P.cfg.capacity_blocks;
   const int Pc = rq.chain[h];
   const int m0 = rq.m[h];

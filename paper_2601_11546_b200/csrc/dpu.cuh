@@ -165,7 +165,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
   const int tid = threadIdx.x, lane = tid & 31, warp = opaque_warp();
   const int n_act = c.n_act;
   int n_est = e1 - e0 < kSmallEst ? e1 - e0 : kSmallEst;
-  const int Ssz = (int)cfg.sample_size;
+  const int Ssz = kC ? 8 : (int)cfg.sample_size;  // kC: the default sample size (engine.py:150)
   const int dper = 2 * Ssz - 1;
   // per-warp metadata: lane e holds relQuery e0 + e
   int a = 0, base = 0, nunp = 0, ol = 0, mcb = 0, L = 0, dcnt = 0, nj = 0;
@@ -286,7 +286,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       if (lane == 0) ratios_sequential(P, T, S, e0, n_est, n_act);
     } else {
       if (lane < n_est && own) {  // sample_cache_miss_ratio (prefix_cache.py:141-169)
-        const long long mh = cfg.block_size * (long long)mcb;  // exact utok = tok - B*m
+        const long long mh = (kC ? 16 : cfg.block_size) * (long long)mcb;  // exact utok = tok - B*m
         double ratio = 0.0;
         if (nunp > 0) {
           long long usum = 0, tsum = 0;

@@ -185,7 +185,8 @@ __device__ __forceinline__ double world_duration(const Params& P, const TraceDev
 }
 
 // kC: the common configuration, fixed at compile time (a DPU policy, tau = inf,
-// no world-model noise, no waiting-order recording, one shard, decision log on):
+// no world-model noise, no waiting-order recording, one shard, decision log on,
+// the default block size 16 and sample size 8):
 // the checks for everything else leave the iteration's instruction stream.
 template <bool kFast, bool kC>
 __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
@@ -423,7 +424,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       const int pend = rq.off[h + 1] - base_row;
       const long long room = cfg.max_num_seqs - c.n_run;
       J = room <= 0 ? 0 : (int)(pend < room ? pend : room);
-      mh = (int)(cfg.block_size * (long long)rq.m[h]);
+      mh = (int)((kC ? 16 : cfg.block_size) * (long long)rq.m[h]);
       olh = rq.ol[h];
     }
     const long long headroom = cfg.cap - c.kv;
@@ -529,7 +530,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
     const int n_run0 = c.n_run;
     const int ol = rq.ol[h];
     long long ut = 0;
-    const bool fast = prefill_fast(P, T, S, h, n, S.cand_tok, ut);
+    const bool fast = prefill_fast<kC>(P, T, S, h, n, S.cand_tok, ut);
     phase_mark(c, 9);
     if (tid == 0) {
       bool ok = c.status == RS_RUNNING;
@@ -1581,7 +1582,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;
   // the common configuration's specialised kernel (see iterate)
   e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && !cfg->record_order &&
-              shard_world == 1 && cfg->log_decisions;
+              shard_world == 1 && cfg->log_decisions && cfg->block_size == 16 && cfg->sample_size == 8;
   for (auto& h : e->traces) e->common = e->common && h.dev.log_cap > 0;
   cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce == cudaSuccess)
