@@ -998,6 +998,11 @@ struct HostTrace {
   void* arena_alloc = nullptr;  // cudaMallocAsync (pool) allocation
   size_t arena_cap = 0, arena_used = 0;
   double* noise_buf = nullptr;  // rs_engine_set_noise
+  // small traces: arena contents are composed in a host image and uploaded in
+  // one copy per flush (stage_flush) instead of a copy / memset per buffer
+  bool staging = false;
+  std::vector<unsigned char> stage;
+  size_t staged_lo = 0;  // arena bytes [staged_lo, arena_used) not uploaded yet
   std::vector<int> zorder;      // every relQuery in the static waiting order
 };
 
@@ -1028,11 +1033,42 @@ int arena_reserve(HostTrace& h, size_t bytes) {
   return RS_OK;
 }
 
+int stage_flush(HostTrace& h) {  // upload the staged arena bytes composed since the last flush
+  if (!h.staging || h.arena_used <= h.staged_lo) return RS_OK;
+  const cudaError_t e = cudaMemcpy(h.arena + h.staged_lo, h.stage.data() + h.staged_lo, h.arena_used - h.staged_lo,
+                                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("staged upload: ") + cudaGetErrorString(e));
+  h.staged_lo = h.arena_used;
+  return RS_OK;
+}
+
 template <typename T>
 int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_byte = -1, bool async = false) {
   if (n == 0) n = 1;
   void* q = nullptr;
   const size_t nb = (n * sizeof(T) + 255) & ~(size_t)255;
+  if (h.staging && h.arena && h.arena_used + nb <= h.arena_cap && !src && fill_byte >= 0 && nb >= (64u << 10)) {
+    // a large fill (the decision-log ring): flush what is composed, fill on the device
+    int rc = stage_flush(h);
+    if (rc) return rc;
+    q = h.arena + h.arena_used;
+    h.arena_used += nb;
+    h.staged_lo = h.arena_used;
+    h.bytes += (long long)(n * sizeof(T));
+    const cudaError_t e = cudaMemsetAsync(q, fill_byte, n * sizeof(T), 0);
+    if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+    *p = (T*)q;
+    return RS_OK;
+  }
+  if (h.staging && h.arena && h.arena_used + nb <= h.arena_cap) {  // composed on the host
+    const size_t at = h.arena_used;
+    h.arena_used += nb;
+    h.bytes += (long long)(n * sizeof(T));
+    if (src) memcpy(h.stage.data() + at, src, n * sizeof(T));
+    else if (fill_byte >= 0) memset(h.stage.data() + at, fill_byte, n * sizeof(T));
+    *p = (T*)(h.arena + at);
+    return RS_OK;
+  }
   if (h.arena && h.arena_used + nb <= h.arena_cap) {
     q = h.arena + h.arena_used;
     h.arena_used += nb;
@@ -1164,6 +1200,11 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
                         (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
                         12 * (size_t)(R + 1) + 8 + 36 * 256;
     TRY(arena_reserve(h, need));
+    if (N < (1LL << 16)) {  // small trace: compose the arena on the host, upload it in two copies
+      h.staging = true;
+      h.stage.assign(need, 0);
+      h.staged_lo = 0;
+    }
   }
   // admission order == trace order: the caller's rows go up now (stream 0, asynchronous
   // from page-locked memory) while the host threads below validate them
@@ -1340,6 +1381,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       PemModel m{h.pol.alpha_p, h.pol.beta_p, h.pol.alpha_d, h.pol.beta_d, cfg->cap, cfg->max_num_seqs,
                  cfg->max_num_batched_tokens};
       const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
+      TRY(stage_flush(h));  // the kernel reads the rows and writes fsprio
       first_sight_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d.tok, m, (double*)d.fsprio);
       cudaError_t ke = cudaGetLastError();
       if (ke == cudaSuccess) ke = cudaDeviceSynchronize();
@@ -1429,8 +1471,11 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   rc = dalloc(h, &d.ctl, 1, ctl);
   free(ctl);
   if (rc) return rc;
+  rc = stage_flush(h);
+  h.staging = false;
+  std::vector<unsigned char>().swap(h.stage);
 #undef TRY
-  return RS_OK;
+  return rc;
 }
 
 // Another shard's replica of a built trace (sharded pool, all shards in one
