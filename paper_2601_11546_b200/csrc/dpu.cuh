@@ -160,7 +160,7 @@ __device__ __noinline__ long long floyd_tok_sum_any(const int* tok, const unsign
 template <bool kC>
 __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const PemModel& pm, int e0, int e1) {
   Ctl& c = S.c;
-  const RqView& rq = S.rq;
+  const RqView rq = S.rq;  // by value: the table pointers stay in registers across the barriers
   const rs_config& cfg = P.cfg;
   const int tid = threadIdx.x, lane = tid & 31, warp = opaque_warp();
   const int n_act = c.n_act;
