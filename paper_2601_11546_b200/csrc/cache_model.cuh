@@ -205,7 +205,7 @@ template <bool kC>
 __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int h, int n, const int* tokv,
                              long long& ut_out) {
   Ctl& c = S.c;
-  const RqView& rq = S.rq;
+  const RqView rq = S.rq;  // by value: the table pointers stay in registers across the barriers
   const int tid = threadIdx.x;
   const long long B = kC ? 16 : P.cfg.block_size;  // kC: the default block size (engine.py:152)
   const long long C = P.cfg.capacity_blocks;
