@@ -48,7 +48,7 @@ PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dp
 WINDOW_START = 5
 #: dram__bytes_read.sum + dram__bytes_write.sum per engine_kernel launch (250 iterations) from the
 #: committed `ncu --set full` capture (profiles/r1_engine_kernel.md); None until measured
-TRAFFIC_PER_LAUNCH = 298240.0
+TRAFFIC_PER_LAUNCH = 297216.0
 
 
 def parse():
