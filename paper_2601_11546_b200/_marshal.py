@@ -147,10 +147,12 @@ def marshal_trace(trace: ArrivalTrace, block_size: int, policy: str, policy_mode
 def _static_priorities(trace: ArrivalTrace, model, sp_fns) -> np.ndarray:
     """static_relquery_prio per relQuery (engine.py:255-264, priority.py:221-235).
 
-    The reference sums with the builtin ``sum``, which since CPython 3.12 uses
-    Neumaier-compensated float summation; `_py_sum` restates that loop so the
-    static priorities are bit-identical.  Default mappings are alpha_p*tok and
-    alpha_d*ol of the policy model (engine.py:259-261).
+    The reference sums with the builtin ``sum`` (Neumaier-compensated since
+    CPython 3.12, plain left-to-right before), so this does too: the static
+    priorities are bit-identical under the running interpreter.  Default
+    mappings are alpha_p*tok and alpha_d*ol of the policy model
+    (engine.py:259-261).  Any sign is allowed (the device orders priorities by
+    an order-preserving key, engine_state.cuh okey()).
     """
     c = trace.columns()
     out = np.zeros(c.num_relqueries, np.float64)
@@ -159,30 +161,12 @@ def _static_priorities(trace: ArrivalTrace, model, sp_fns) -> np.ndarray:
         ol = np.repeat(c.output_limit.astype(np.float64), np.diff(c.row_off))
         vals = (model.alpha_p * c.tok.astype(np.float64) + model.alpha_d * ol).tolist()
         for q in range(c.num_relqueries):
-            out[q] = _py_sum(vals[off[q]:off[q + 1]])
+            out[q] = sum(vals[off[q]:off[q + 1]])  # the running interpreter's sum, as the reference's
         return out
     l1, l2 = sp_fns
     for q, rq in enumerate(trace.entries):
         out[q] = float(sum(l1(r.tok) + l2(r.output_limit) for r in rq.requests))
     return out
-
-
-def _py_sum(xs) -> float:
-    """CPython >= 3.12 ``sum(floats, 0)``: int start, then Neumaier compensation."""
-    if not xs:
-        return 0.0
-    f = xs[0]
-    comp = 0.0
-    for x in xs[1:]:
-        t = f + x
-        if abs(f) >= abs(x):
-            comp += (f - t) + x
-        else:
-            comp += (x - t) + f
-        f = t
-    if comp and math.isfinite(comp):
-        f += comp
-    return float(f)
 
 
 def make_config(cfg, policy: str, record_order: bool = False) -> _abi.Config:

@@ -137,7 +137,7 @@ __device__ __noinline__ void record_waiting_order(const TraceDev& T, Shared& S, 
     int v[1] = {w ? 1 : 0}, tot[1];
     block_scan32<1>(v, S.s32, tot);
     if (w) {
-      S.ord.key[n + v[0] - 1] = dbits(rq.prio[a]);
+      S.ord.key[n + v[0] - 1] = okey(rq.prio[a]);
       S.ord.rank[n + v[0] - 1] = a;
     }
     n += tot[0];
@@ -312,7 +312,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         const unsigned em = __ballot_sync(kFull, elig);
         if (em) {
           idx = __shfl_sync(kFull, a, __ffs(em) - 1);
-          key = dbits(rq.prio[idx]);
+          key = okey(rq.prio[idx]);
           break;
         }
         i0 += 32;
@@ -327,7 +327,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
         for (int j = lane; j < c.n_act; j += 32) {
           const int a = c.act[j];
           if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (kC || T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
-            const unsigned long long k = dbits(rq.prio[a]);
+            const unsigned long long k = okey(rq.prio[a]);
             if (k < key || (k == key && a < idx)) {
               key = k;
               idx = a;
@@ -360,7 +360,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       for (int a = tid; a < c.n_admitted; a += kThreads) {
         if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
           ++w;
-          const unsigned long long k = dbits(rq.prio[a]);
+          const unsigned long long k = okey(rq.prio[a]);
           if (k < key) {  // ranks visited in increasing order: strict < keeps the smallest rank
             key = k;
             idx = a;
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(kThreads) waiting_argmin_kernel(long long n, c
   for (long long a = threadIdx.x; a < n; a += kThreads) {
     if (waiting[a]) {
       ++w;
-      const unsigned long long k = dbits(prio[a]);
+      const unsigned long long k = okey(prio[a]);
       if (k < key) {
         key = k;
         idx = (int)a;
@@ -1174,7 +1174,11 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     ol[a] = v.output_limit[t];
     chain[a] = v.chain_blocks ? v.chain_blocks[t] : 0;
     relid[a] = v.rel_id[t];
-    if (v.static_prio) sprio[a] = v.static_prio[t];
+    if (v.static_prio) {  // any number: the waiting order compares okey() keys; -0.0 ties with 0.0 there
+      const double p = v.static_prio[t];
+      if (p != p) return fail(RS_EINVAL, "static priority is NaN");
+      sprio[a] = p == 0.0 ? 0.0 : p;
+    }
     const long long lo = v.row_off[t], hi = v.row_off[t + 1];
     if (hi < lo) return fail(RS_EINVAL, "row_off must be non-decreasing");
     if (ol[a] <= 0) return fail(RS_EINVAL, "output_limit must be positive");
@@ -1423,11 +1427,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
         if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("first-sight readback: ") + cudaGetErrorString(ce));
       }
       std::vector<std::pair<unsigned long long, int>> zk(R);  // (priority bits, rank): stable by the rank
-      for (long long a = 0; a < R; ++a) {
-        unsigned long long b;
-        memcpy(&b, &zp[a], 8);
-        zk[a] = {b, (int)a};
-      }
+      for (long long a = 0; a < R; ++a) zk[a] = {okey(zp[a]), (int)a};  // the device's key order
       std::sort(zk.begin(), zk.end());
       std::vector<int> z(R);
       for (long long i = 0; i < R; ++i) z[i] = zk[i].second;
@@ -2003,8 +2003,9 @@ int rs_waiting_argmin(const double* priority, const uint8_t* waiting, int64_t n,
                       int64_t* count) {
   if (n < 0 || n > 0x7FFFFFF0LL || (n && (!priority || !waiting)) || !head || !count)
     return fail(RS_EINVAL, "bad waiting-order input");
-  for (long long a = 0; a < n; ++a)  // the bit order equals the value order for these only
-    if (waiting[a] && !(priority[a] >= 0.0)) return fail(RS_EINVAL, "priorities must be non-negative numbers");
+  for (long long a = 0; a < n; ++a)  // okey orders every number; -0.0 would sort before +0.0
+    if (waiting[a] && (priority[a] != priority[a] || (priority[a] == 0.0 && std::signbit(priority[a]))))
+      return fail(RS_EINVAL, "priorities must be numbers (and not -0.0)");
   RS_CUDA(cudaSetDevice(device));
   double* d_p = nullptr;
   unsigned char* d_w = nullptr;

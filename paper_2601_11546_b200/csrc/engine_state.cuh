@@ -12,6 +12,7 @@
 // table live in shared memory (RqView points at either copy).
 #pragma once
 #include <stdint.h>
+#include <string.h>
 
 #include "../../include/relserve.h"
 #include "block.cuh"
@@ -248,8 +249,21 @@ struct Shared {
   // relQuery table follows (dynamic shared memory) when rq_in_smem
 };
 
-__device__ __forceinline__ unsigned long long dbits(double x) {
-  return (unsigned long long)__double_as_longlong(x);
+// Order-preserving 64-bit key of a priority: unsigned comparison of okey(x)
+// equals numeric comparison of x for every non-NaN double (negative values:
+// all bits flipped; others: sign bit set).  The engine's own priorities are
+// non-negative, but sp's user-supplied static priorities may be negative
+// (priority.py:221-235).  -0.0 never reaches the device (the host
+// canonicalises static priorities; PEM sums start at +0.0).  Host twin:
+// engine.cu order_key().
+__host__ __device__ __forceinline__ unsigned long long okey(double x) {
+#ifdef __CUDA_ARCH__
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+#else
+  unsigned long long b;
+  memcpy(&b, &x, 8);
+#endif
+  return b ^ ((unsigned long long)((long long)b >> 63) | 0x8000000000000000ULL);
 }
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7FF8000000000000LL); }

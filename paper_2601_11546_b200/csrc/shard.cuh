@@ -82,7 +82,7 @@ __device__ bool shard_exchange(const TraceDev& T, Shared& S, unsigned long long&
   for (int j = tid; j < n_act; j += kThreads) {
     const int a = c.act[j];
     if (a % W == me) {
-      const unsigned long long v = dbits(rq.prio[a]);
+      const unsigned long long v = (unsigned long long)__double_as_longlong(rq.prio[a]);  // raw bits: decoded below
       for (int d = 0; d < W; ++d) {
         if (d == me) continue;
         unsigned long long* w = T.peers[d][2 * me + par].w + 3 + 2 * j;

@@ -154,11 +154,17 @@ _ABA_PHASES = (2, 3, 11, 12)
 
 class _DecisionLog(list):
     """RunResult.decision_log (engine.py:64-74, 419-433): a list of
-    DecisionLogEntry built from the device records on first use."""
+    DecisionLogEntry built from the device records -- at once for logs up to
+    `EAGER` entries, else on first use (every list method, comparison and
+    mutator fills it first)."""
+
+    EAGER = 1024
 
     def __init__(self, recs: np.ndarray):
         super().__init__()
         self._recs = recs
+        if recs is None or len(recs) <= self.EAGER:
+            self._fill()
 
     def _fill(self):
         recs, self._recs = self._recs, None
@@ -180,8 +186,10 @@ class _DecisionLog(list):
             self._fill()
 
 
-for _name in ("__len__", "__iter__", "__getitem__", "__contains__", "__eq__", "__repr__", "__reversed__",
-              "__bool__", "index", "count", "copy", "__add__", "__mul__"):
+for _name in ("__len__", "__iter__", "__getitem__", "__contains__", "__eq__", "__ne__", "__lt__", "__le__",
+              "__gt__", "__ge__", "__repr__", "__reversed__", "__bool__", "index", "count", "copy", "__add__",
+              "__radd__", "__mul__", "__rmul__", "__iadd__", "__imul__", "__setitem__", "__delitem__", "append",
+              "extend", "clear", "sort", "insert", "pop", "remove", "reverse", "__reduce_ex__", "__sizeof__"):
     if hasattr(list, _name):
         def _wrap(name=_name):
             base = getattr(list, name)
@@ -340,21 +348,18 @@ class Engine:
         done = 0
         while True:
             it0 = self.iteration
-            ne.step(max_iterations - done, self.stream)
+            # one launch runs at most a ring's worth of iterations; its records are read
+            # before the next launch can overwrite them
+            ne.step(min(max_iterations - done, self.chunk_iterations), self.stream)
             st = ne.status(self.stream)[0]
             self.iteration = st.iterations
             done += st.iterations - it0
-            # a launch that ran out of noise draws stops early, still running
-            if (self._noise_rng is None or st.status != _abi.RS_RUNNING or st.batches < len(self._noise)
-                    or done >= max_iterations):
+            self._read_records(st)
+            if st.status != _abi.RS_RUNNING or done >= max_iterations:
                 break
-            self._extend_noise(len(self._noise))
-        if self.config.log_decisions and st.n_log > self._n_read:
-            self._records.append(ne.read_log(0, self._n_read, st.n_log - self._n_read))
-            if self._record_order:
-                self._orders.append(ne.read_order(0, self._n_read, st.n_log - self._n_read,
-                                                  self.trace.columns().num_relqueries))
-            self._n_read = st.n_log
+            # a launch that ran out of noise draws stops early, still running
+            if self._noise_rng is not None and st.batches >= len(self._noise):
+                self._extend_noise(len(self._noise))
         self._status = st
         self.iteration = st.iterations
         self.clock = st.clock
@@ -362,6 +367,14 @@ class Engine:
         return st
 
     _n_read = 0
+
+    def _read_records(self, st) -> None:
+        if self.config.log_decisions and st.n_log > self._n_read:
+            self._records.append(self._native.read_log(0, self._n_read, st.n_log - self._n_read))
+            if self._record_order:
+                self._orders.append(self._native.read_order(0, self._n_read, st.n_log - self._n_read,
+                                                            self.trace.columns().num_relqueries))
+            self._n_read = st.n_log
 
     def run(self) -> RunResult:
         t0 = time.perf_counter()

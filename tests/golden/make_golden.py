@@ -40,7 +40,7 @@ from relsim.engine import Engine, EngineConfig, SimulationAborted  # noqa: E402
 from relsim.priority import SchedulerConstraints  # noqa: E402
 from relsim.workload import ArrivalTrace, RelQuery, Request, TraceConfig, generate_trace, load_trace  # noqa: E402
 
-from golden_util import GOLDEN_DIR, digest_entries  # noqa: E402
+from golden_util import GOLDEN_DIR, SP_FNS, digest_entries  # noqa: E402
 
 TEST_MODEL = (0.001, 0.02, 0.0002, 0.015)  # pkg/tests/test_engine.py:11
 
@@ -167,6 +167,8 @@ def engine_config(c):
     kw = {}
     if cons:
         kw["constraints"] = SchedulerConstraints(*cons)
+    if "sp_fns" in cc:
+        cc["sp_priority_fns"] = SP_FNS[cc.pop("sp_fns")]
     if "tau" in cc:
         cc["tau"] = float(cc["tau"])
     kw.update(cc)
@@ -262,6 +264,11 @@ CASES = {
     "cfg1_sp": dict(spec=CFG1, policy="sp", world="opt-13b-like"),
     "cfg1_pp": dict(spec=CFG1, policy="relserve-pp", world="opt-13b-like"),
     "cfg1_dp": dict(spec=CFG1, policy="relserve-dp", world="opt-13b-like"),
+    # sp with user priority functions of either sign (priority.py:221-235)
+    "sp_negative": dict(spec=gen({"num_relqueries": 30, "size_range": [1, 40], "rate": 4.0, "seed": 41}),
+                        policy="sp", world="opt-13b-like", config={"sp_fns": "neg_mixed"}),
+    "sp_negative_only": dict(spec=gen({"num_relqueries": 25, "size_range": [1, 30], "rate": 6.0, "seed": 42}),
+                             policy="sp", world=list(TEST_MODEL), config={"sp_fns": "neg_only"}),
     # tight constraints (pkg/tests/test_engine.py:181-195)
     "tight_relserve": dict(spec=gen({"num_relqueries": 25, "size_range": [1, 30], "rate": 5.0, "seed": 21}),
                            policy="relserve", world=list(TEST_MODEL), config=TIGHT),

@@ -41,6 +41,14 @@ def digest_columns(c) -> str:
                          np.diff(c.row_off), c.tok, c.out)
 
 
+#: named `EngineConfig.sp_priority_fns` pairs (golden configs say {"sp_fns": name}):
+#: static priorities of either sign, so the waiting order is checked below zero too
+SP_FNS = {
+    "neg_mixed": (lambda tok: -0.001 * tok, lambda ol: 0.3 - 0.02 * ol),
+    "neg_only": (lambda tok: -1.0 - 0.0005 * tok, lambda ol: -0.01 * ol),
+}
+
+
 def load_golden(name: str) -> dict:
     p = GOLDEN_DIR / f"{name}.json.gz"
     with gzip.open(p, "rt") as f:

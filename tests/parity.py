@@ -9,7 +9,7 @@ import math
 
 import numpy as np
 
-from golden_util import digest_columns
+from golden_util import SP_FNS, digest_columns
 from paper_2601_11546_b200 import _abi
 from paper_2601_11546_b200.cost_model import LinearCostModel, world_preset
 from paper_2601_11546_b200.engine import EngineConfig
@@ -51,6 +51,8 @@ def engine_config(c: dict, window=None) -> EngineConfig:
     cons = c.pop("constraints", None)
     if cons:
         kw["constraints"] = SchedulerConstraints(*cons)
+    if "sp_fns" in c:
+        c["sp_priority_fns"] = SP_FNS[c.pop("sp_fns")]
     if "tau" in c:
         c["tau"] = float(c["tau"])
     kw.update(c)
