@@ -6,13 +6,15 @@ Workload (config 2 of BASELINE.json): 1,000 relQueries x 1,000 rows
 only 13B preset; "Llama-2-13B" maps to it), EngineConfig() defaults, policy
 relserve, engine seed 0.  A *step* is one launch of the persistent scheduler
 kernel that advances the trace by `--iters-per-step` scheduler iterations.
-The window starts at iteration 5 (after admission and the first-sight DPU
-pass); W warm-up steps, then K timed steps, each bracketed
-by CUDA events on the launching stream, with a 256 MiB L2 flush between steps
-(outside the events).  `value` = iterations / summed step time.
+Iterations [0, 5) run first (admission and the first-sight DPU pass, as in
+SURVEY 8d); then W warm-up steps, then K timed steps, each bracketed by CUDA
+events on the launching stream, with a 256 MiB L2 flush between steps
+(outside the events).  The timed window is iterations [5 + W*I, 5 + (W+K)*I),
+printed as config.window_start/end_iteration -- the same window the reference
+arm times.  `value` = iterations / summed step time.
 
-`e2e` runs the same window through the public API (`Engine` over host
-arrays): trace upload, every step's launch, status and decision-record
+`e2e` runs iterations [0, window end) through the public API (`Engine` over
+host arrays): trace upload, every step's launch, status and decision-record
 readback, and the final ledger/request readback are inside the wall-clock
 timed region.
 
@@ -46,9 +48,58 @@ PHASES = ("admit", "dpu_other", "order", "decision", "execute", "dpu_setup", "dp
           "dpu_pem", "fp_evict_post", "prefill_post", "cand_decode", "cand_prefill", "fp_scan", "fp_stage",
           "dpu_ratio", "p16", "p17", "p18", "p19", "p20", "p21", "p22")
 WINDOW_START = 5
-#: dram__bytes_read.sum + dram__bytes_write.sum per engine_kernel launch (250 iterations) from the
-#: committed `ncu --set full` capture (profiles/r1_engine_kernel.md); None until measured
-TRAFFIC_PER_LAUNCH = 297216.0
+#: per-config ncu numbers of the dominant kernel from the committed `ncu --set full` capture
+#: (dram__bytes_read.sum + dram__bytes_write.sum per launch; tools/ncu_traffic.py writes it)
+TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
+L2_NOTE = ("GPU arm: a 256 MiB buffer is written between timed steps (outside the events); "
+           "CPU arm: not applicable")
+
+
+def traffic(cfg_id: str, iters_per_step: int):
+    """ncu DRAM bytes per launch of the bench's kernel for this config, scaled to this launch
+    size, with the capture it comes from (None if no capture of this config is committed)."""
+    try:
+        d = json.loads(TRAFFIC_FILE.read_text()).get(f"config{cfg_id}")
+    except (OSError, ValueError):
+        d = None
+    if not d:
+        return None, None
+    per_iter = d["dram_bytes_per_launch"] / d["iters_per_launch"]
+    return per_iter * iters_per_step, d
+
+
+def window_stats(recs, comp, c, lo: int, hi: int) -> dict:
+    """The workload at the timed window [lo, hi) from a run's decision records (all
+    iterations from 0) and per-request completion iterations: requests waiting at lo, and the
+    mean live requests / relQueries over the window (B_iter = 6 N_live + 56 R_live)."""
+    it = recs["iteration"]
+    clock_lo = float(recs["clock"][np.searchsorted(it, lo)]) if len(it) and lo <= it[-1] else math.inf
+    sizes = np.diff(c.row_off)
+    adm_rq = c.arrival <= clock_lo  # admitted by iteration lo (engine.py:243-249)
+    n_adm = int(sizes[adm_rq].sum())
+    pf = (recs["action"] == 0) & (it < lo)
+    pending = n_adm - int(recs["batch_n"][pf].sum())
+    ts = np.arange(lo, hi)
+    done = np.sort(comp[comp >= 0])
+    n_live = n_adm - np.searchsorted(done, ts, side="left")  # rows done before t are not live at t
+    rq_of = np.repeat(np.arange(c.num_relqueries), sizes)
+    last = np.full(c.num_relqueries, -1, np.int64)
+    np.maximum.at(last, rq_of, np.where(comp < 0, np.iinfo(np.int64).max // 2, comp))
+    rq_done = np.sort(last[adm_rq & (sizes > 0)])
+    r_live = int((adm_rq & (sizes > 0)).sum()) - np.searchsorted(rq_done, ts, side="left")
+    return {"pending_requests_start": int(pending), "live_requests_mean": float(n_live.mean()),
+            "live_relqueries_mean": float(r_live.mean())}
+
+
+def b_iter(ws: dict) -> float:
+    """SURVEY 8d's declared algorithmic bytes per iteration: 6 N_live + 56 R_live."""
+    return 6.0 * ws["live_requests_mean"] + 56.0 * ws["live_relqueries_mean"]
+
+
+def config_dict(wname: str, I: int, lo: int, hi: int, ws: dict) -> dict:
+    """The `config` of both arms' lines (identical keys and values for the same run shape)."""
+    return {"workload": wname, "iters_per_step": I, "window_start_iteration": lo, "window_end_iteration": hi,
+            "pending_requests_start": ws["pending_requests_start"], "l2": L2_NOTE}
 
 
 def parse():
@@ -281,9 +332,12 @@ def run_ours(args, ws, rank, local):
     alg_window = st.alg_bytes - ab0
     assert st.status == _abi.RS_RUNNING, f"trace ended inside the window (status {st.status})"
     recs = ne.read_log(0, n_read, st.n_log - n_read)
+    recs_all = ne.read_log(0, 0, st.n_log)
     gen, pre, comp, prio = ne.read_requests(0, trace.columns().num_requests)
     pending_end = int((pre == 0).sum())
     ne.close()
+    it1 = it0 + iters
+    wstats = window_stats(recs_all, comp, trace.columns(), it0, it1)
     t_ms = sum(step_ms)
     t_max = max_over_ranks(t_ms, ws, dev)
     # independent traces: every rank's iterations count; one sharded pool: its iterations once
@@ -294,11 +348,13 @@ def run_ours(args, ws, rank, local):
     avg_launch_s = (t_ms / args.steps) / 1e3
     peak, peak_kind = peaks()
     achieved = per_launch_bytes / avg_launch_s / 1e9
+    achieved_b_iter = b_iter(wstats) * (iters / args.steps) / avg_launch_s / 1e9
+    traffic_launch, traffic_src = traffic(args.config, I)
 
     # ---- end to end through the public API (host buffers, copies inside)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, srank)
+        e2e = e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, srank, it1)
 
     out = None
     if rank == 0:
@@ -318,21 +374,27 @@ def run_ours(args, ws, rank, local):
             "vs_baseline": None,
             "dtype": "f64+int32",
             "data": "synthetic (relsim generate_trace, count-identical to the reference generator)",
-            "config": {"workload": wname, "iters_per_step": I, "window_start_iteration": WINDOW_START,
-                       "shards": shards, "shard_mode": ("one per GPU (NVLink P2P mailboxes)" if pool and ws > 1
-                                                        else "CTAs of one launch on one GPU" if pool else None),
-                       "pending_requests_start": pending0, "pending_requests_end": pending_end,
-                       "l2": "256 MiB buffer written between timed steps (outside the events)",
-                       "traces_per_gpu": 1 if not pool else None},
+            "config": config_dict(wname, I, it0, it1, wstats),
+            "run": {"shards": shards, "shard_mode": ("one per GPU (NVLink P2P mailboxes)" if pool and ws > 1
+                                                      else "CTAs of one launch on one GPU" if pool else None),
+                    "requests_total": pending0, "pending_requests_end": pending_end,
+                    "live_requests_mean": wstats["live_requests_mean"],
+                    "live_relqueries_mean": wstats["live_relqueries_mean"],
+                    "traces_per_gpu": 1 if not pool else None},
             "iterations_timed": int(total_iters),
             "e2e": e2e,
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": TRAFFIC_PER_LAUNCH, "peak_source": peak_kind,
+                         "frac": achieved / peak, "traffic": traffic_launch, "peak_source": peak_kind,
                          "alg_bytes_per_iter": alg_window / max(1, iters),
-                         "note": "latency-bound: one dependent iteration chain per trace; bytes = the "
-                                 "device-counted algorithmic bytes (DESIGN.md); traffic = ncu dram bytes per "
-                                 "launch of the committed profile (profiles/)"},
+                         "b_iter": b_iter(wstats), "achieved_b_iter": achieved_b_iter,
+                         "frac_b_iter": achieved_b_iter / peak,
+                         "traffic_source": traffic_src,
+                         "note": "latency-bound: one dependent iteration chain per trace. frac: the bytes this "
+                                 "design moves, counted on the device (DESIGN.md 5); frac_b_iter: SURVEY 8d's "
+                                 "declared B_iter = 6 N_live + 56 R_live (a design rescanning every live row each "
+                                 "iteration) at the same iteration rate; traffic: ncu dram bytes per launch "
+                                 "(profiles/traffic.json)"},
             "clocks": clk.summary(),
             "phase_cycles_per_iter": dict(zip(PHASES, [round(x / max(1, iters), 1) for x in ph])),
             "iteration_mix": {"prefill": int((recs["action"] == 0).sum()), "decode": int((recs["action"] == 1).sum()),
@@ -348,7 +410,7 @@ def run_ours(args, ws, rank, local):
 E2E_REPEATS = 3
 
 
-def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, srank):
+def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, srank, it_end):
     """The bench window through the public `Engine` API from host arrays: trace upload and
     first-sight kernel (engine creation), every step's launch + status + decision-record
     readback, and the final ledger / completion readback, wall-clock timed."""
@@ -376,8 +438,8 @@ def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, s
         t1 = time.perf_counter()
         eng.step(WINDOW_START)
         t15 = time.perf_counter()
-        for _ in range(args.steps):
-            eng.step(I)
+        while eng.iteration < it_end:  # up to the device window's last iteration, I per step
+            eng.step(min(I, it_end - eng.iteration))
         t2 = time.perf_counter()
         eng._collect(0.0)
         torch.cuda.synchronize(dev)
@@ -394,16 +456,18 @@ def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, s
                                       "collect_ms": 1e3 * (t3 - t2)}})
     med = sorted(runs, key=lambda r: r["value"])[len(runs) // 2]
     h2d = sum(v.nbytes for v in m.arrays.values() if v is not None)
+    n_steps = -(-(it_end - WINDOW_START) // I) + 1  # launches of the run (the first: iterations [0, 5))
     d2h_step = I * 96 + 128
     d2h_final = c.num_requests * 4 + c.num_relqueries * 32
     return {"value": med["value"], "unit": "iters/s",
-            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / args.steps),
+            "h2d_bytes_per_step": int(h2d / n_steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / n_steps),
+            "window": [0, it_end],
             "iterations": med["iterations"], "wall_s": med["wall_s"], "breakdown_ms": med["breakdown_ms"],
             "runs": [{"value": round(r["value"], 1), **{k: round(v, 2) for k, v in r["breakdown_ms"].items()}}
                      for r in runs],
             "statistic": f"median of {E2E_REPEATS} runs after one untimed warm-up run",
-            "includes": "trace upload, iterations 0..window end (incl. first-sight DPU), per-step record "
-                        "readback, final ledger/completion readback"}
+            "includes": "trace upload, iterations 0..the device window's end (incl. first-sight DPU), per-step "
+                        "record readback, final ledger/completion readback"}
 
 
 def cpu_baseline(args, trace, world, cfg, iters=None):
@@ -449,11 +513,13 @@ def run_reference(args, ws, rank):
     lo = WINDOW_START + args.warmup * per_step
     win = r.iter_wall[lo:n]
     value = float(len(win) / win.sum())
+    wstats = window_stats(r.log, r.completion_iter, trace.columns(), lo, n)
     return {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": float(win.sum() / args.steps * 1e3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-        "config": {"workload": wname, "iters_per_step": per_step, "window_start_iteration": lo},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+int32",
+        "data": "synthetic (relsim generate_trace, count-identical to the reference generator)",
+        "config": config_dict(wname, per_step, lo, n, wstats),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "port",
                          "sample": f"oracle/ C restatement of relsim Engine.run, iterations [{lo}, {n})",

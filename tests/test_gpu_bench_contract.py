@@ -34,6 +34,7 @@ def test_bench_line_ours():
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor") and r["unit"] == "GB/s" and r["peak"] > 0
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert r["frac_b_iter"] == pytest.approx(r["achieved_b_iter"] / r["peak"]) and r["b_iter"] > 0
     c = d["cpu_baseline"]
     assert c["value"] > 0 and c["cores"] >= 1 and c["kind"] in ("port", "reference") and c["sample"]
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
@@ -44,3 +45,14 @@ def test_bench_line_reference_arm():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "iters/s"
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["kind"] in ("port", "reference")
+
+
+def test_both_arms_time_the_same_window():
+    """Same trace, same window, same config dict: the driver's same_config check."""
+    ours = _bench("--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline")
+    ref = _bench("--impl", "reference", "--steps", "2", "--warmup", "3")
+    assert ours["config"] == ref["config"]
+    c = ours["config"]
+    assert c["window_start_iteration"] == 5 + 3 * c["iters_per_step"]
+    assert c["window_end_iteration"] == c["window_start_iteration"] + 2 * c["iters_per_step"]
+    assert 0 < c["pending_requests_start"] <= 1_000_000
