@@ -66,8 +66,9 @@ typedef struct {
   int64_t iteration_limit;
   int32_t log_decisions;          /* record one rs_iter_record per iteration */
   int32_t policy;                 /* RS_POLICY_* */
-  int32_t record_order;           /* parity mode: also record the full waiting order per iteration
-                                     (rs_engine_read_order); needs log_decisions, <= 4096 relQueries */
+  int32_t record_order;           /* parity mode: also snapshot every iteration's priority update
+                                     (rs_engine_read_dpu) and waiting order (rs_engine_read_order);
+                                     needs log_decisions; any number of relQueries */
   int32_t reserved;
 } rs_config;
 
@@ -198,10 +199,28 @@ int rs_engine_read_log(rs_engine* e, int32_t t, int64_t first, int64_t count, rs
  * (priority, arrival, rel_id)), as trace-order relQuery indices.  Row i of
  * out has `stride` = num_relqueries entries; its first record.n_waiting are
  * the queue, the rest -1.  The hot path never sorts: it only needs the head
- * and the length (a top-1 over a static order).
+ * and the length (a top-1 over a static order); the order is
+ * rebuilt from the iteration's priority snapshot by the device radix sort
+ * (rs_sort_pairs' kernels) when read.  count <= the log capacity; read the
+ * rows of a launch before the next launch.
  */
 int rs_engine_read_order(rs_engine* e, int32_t t, int64_t first, int64_t count, int32_t* out);
 
+/*
+ * Parity mode (cfg.record_order): the Dynamic Priority Updater's records of
+ * iterations [first, first+count) (priority.py:287-315).  Row i of values /
+ * flags has num_relqueries entries in trace order: the relQuery's priority
+ * after the update (NaN if not admitted yet) and RS_SNAP_* bits; rng[i] is the
+ * DPU generator state after the update.  Any pointer may be NULL.
+ */
+enum {
+  RS_SNAP_ESTIMATED = 1,  /* recomputed this iteration (PriorityRecord.reused == False) */
+  RS_SNAP_OVERRIDE = 2,   /* starvation override applied (priority.py:318-339) */
+  RS_SNAP_LIVE = 4,       /* in live_relqueries: admitted and not retired */
+  RS_SNAP_WAITING = 8     /* has pending rows: in the waiting queue */
+};
+int rs_engine_read_dpu(rs_engine* e, int32_t t, int64_t first, int64_t count, double* values, uint8_t* flags,
+                       rs_pcg64_state* rng);
 /* Timestamp ledgers per relQuery in trace order; NaN = None (engine.py:52-61). */
 int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* first_prefill_start,
                            double* last_prefill_end, double* last_decode_end);
@@ -306,8 +325,8 @@ int rs_pem_batch(int64_t n_sets, const int64_t* item_off, const int64_t* utok,
  * len(waiting)): over n relQueries given in admission order -- sorted by
  * (arrival, rel_id), engine.py:211-213 -- the first minimum of `priority`
  * among those with waiting[i] != 0 (*head = -1 if none) and their count.  The
- * engine's own full-scan reduction on the device.  Priorities of waiting
- * entries must be non-negative (every policy's are); EINVAL otherwise.
+ * engine's own full-scan reduction on the device, over the order-preserving
+ * key of each priority (any sign; NaN and -0.0 are EINVAL).
  * Replaces: the `waiting.sort(key=...)` + `waiting[0]` pair of Engine.run.
  */
 int rs_waiting_argmin(const double* priority, const uint8_t* waiting, int64_t n, int32_t device, int64_t* head,
@@ -340,6 +359,18 @@ int rs_arrange(int32_t n_run, const int64_t* run_rel_id, const int64_t* run_outp
  */
 int rs_choice_sequence(rs_pcg64_state* rng, int64_t n_calls, const int64_t* n, const int64_t* k,
                        int64_t* idx_out, int32_t device);
+
+/*
+ * North-star kernel 2 as a unit entry point: stable sort of n (key, value)
+ * pairs by unsigned 64-bit key (equal keys keep their input order) with the
+ * device LSD radix sort the engine uses for its static waiting order and
+ * parity-mode waiting orders (csrc/radix_sort.cuh).  With keys =
+ * order-preserving priority keys and values = admission ranks in rank order
+ * this is `waiting.sort(key=sort_key)` (engine.py:175-176, 277-281).  Host
+ * buffers; synchronous.
+ */
+int rs_sort_pairs(const uint64_t* keys, const int32_t* values, int64_t n, uint64_t* keys_out, int32_t* values_out,
+                  int32_t device);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,9 @@ RS_ENOMEM = 7
 RS_EUNSUPPORTED = 8
 RS_RUNNING = 100
 
+# parity-mode snapshot flags (include/relserve.h RS_SNAP_*)
+SNAP_ESTIMATED, SNAP_OVERRIDE, SNAP_LIVE, SNAP_WAITING = 1, 2, 4, 8
+
 POLICY_IDS = {"fcfs": 0, "sp": 1, "relserve": 2, "relserve-pp": 3, "relserve-dp": 4}
 ACTIONS = ("prefill", "decode", "idle")
 CASES = ("preempt", "internal", "transitional", "forced")

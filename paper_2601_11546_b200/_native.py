@@ -97,6 +97,11 @@ def lib():
     L.rs_engine_set_noise.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]
     L.rs_ipc_close.restype = C.c_int
     L.rs_ipc_close.argtypes = [C.c_void_p]
+    L.rs_engine_read_dpu.restype = C.c_int
+    L.rs_engine_read_dpu.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p]
+    L.rs_sort_pairs.restype = C.c_int
+    L.rs_sort_pairs.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32]
     _lib = L
     return L
 
@@ -108,7 +113,7 @@ EXPORTED_SYMBOLS = (
     "rs_engine_destroy", "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
     "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange", "rs_waiting_argmin",
-    "rs_engine_read_order", "rs_trace_v1_load", "rs_trace_v1_info", "rs_trace_v1_columns", "rs_trace_v1_free",
+    "rs_engine_read_order", "rs_engine_read_dpu", "rs_sort_pairs", "rs_trace_v1_load", "rs_trace_v1_info", "rs_trace_v1_columns", "rs_trace_v1_free",
     "rs_trace_v1_error",
 )
 
@@ -217,6 +222,17 @@ class NativeEngine:
             _check(lib().rs_engine_read_order(self.h, t, first, count, out.ctypes.data))
         return out[:, :R]
 
+    def read_dpu(self, t: int, first: int, count: int, R: int):
+        """Parity mode: the priority update of logged iterations [first, first+count): per
+        iteration and relQuery (trace order) the value and RS_SNAP_* flags, and the DPU
+        generator state after the update (include/relserve.h rs_engine_read_dpu)."""
+        vals = np.full((count, max(R, 1)), np.nan, np.float64)
+        flags = np.zeros((count, max(R, 1)), np.uint8)
+        rng = (_abi.Pcg64State * max(count, 1))()
+        if count:
+            _check(lib().rs_engine_read_dpu(self.h, t, first, count, vals.ctypes.data, flags.ctypes.data, rng))
+        return vals[:, :R], flags[:, :R], [rng[i] for i in range(count)]
+
     def read_ledgers(self, t: int, R: int):
         a, b, c, d = (np.zeros(R, np.float64) for _ in range(4))
         _check(lib().rs_engine_read_ledgers(self.h, t, a.ctypes.data, b.ctypes.data, c.ctypes.data,
@@ -309,6 +325,27 @@ def waiting_argmin(priority, waiting, device=0):
     _check(lib().rs_waiting_argmin(p.ctypes.data if len(p) else None, w.ctypes.data if len(w) else None, len(p),
                                    device, C.byref(head), C.byref(count)))
     return head.value, count.value
+
+
+def sort_pairs(keys, values, device=0):
+    """Stable device radix sort of (uint64 key, int32 value) pairs by key (include/relserve.h
+    rs_sort_pairs, north-star kernel 2)."""
+    k = np.ascontiguousarray(keys, np.uint64)
+    v = np.ascontiguousarray(values, np.int32)
+    if k.shape != v.shape:
+        raise ValueError("keys and values differ in length")
+    ko, vo = np.empty_like(k), np.empty_like(v)
+    _check(lib().rs_sort_pairs(k.ctypes.data if len(k) else None, v.ctypes.data if len(v) else None, len(k),
+                               ko.ctypes.data if len(k) else None, vo.ctypes.data if len(v) else None, device))
+    return ko, vo
+
+
+def priority_keys(prio) -> np.ndarray:
+    """okey() of include/relserve.h's waiting order: uint64 keys whose unsigned order is the
+    numeric order of the priorities (any sign)."""
+    b = np.ascontiguousarray(prio, np.float64).view(np.uint64)
+    neg = (b >> np.uint64(63)).astype(bool)
+    return np.where(neg, ~b, b | np.uint64(1 << 63))
 
 
 def read_trace_v1(path):

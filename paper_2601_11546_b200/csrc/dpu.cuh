@@ -310,17 +310,15 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
       __syncwarp();
       phase_mark(c, 15);
       if (lane == 0 && D > 0) {  // advance the generator past the D values
+        // numpy's next32 buffer: the high half of the last 64-bit output stays in
+        // `uinteger` whether or not it was consumed (an even count leaves it stale)
         if (cnt32 == 0) {
           c.rng.has_uint32 = 0;
         } else {
           c.rng.state_hi = s_end.hi;
           c.rng.state_lo = s_end.lo;
-          if (cnt32 & 1) {
-            c.rng.has_uint32 = 1;
-            c.rng.uinteger = (uint32_t)(out_end >> 32);
-          } else {
-            c.rng.has_uint32 = 0;
-          }
+          c.rng.has_uint32 = cnt32 & 1;
+          c.rng.uinteger = (uint32_t)(out_end >> 32);
         }
       }
     }
@@ -487,10 +485,8 @@ __device__ __forceinline__ rs_pcg64_state advance32(rs_pcg64_state r, long long 
   const U128 s1 = pcg_jump(U128{r.state_hi, r.state_lo}, (unsigned long long)((k + 1) >> 1), jt);
   r.state_hi = s1.hi;
   r.state_lo = s1.lo;
-  if (k & 1) {
-    r.has_uint32 = 1;
-    r.uinteger = (uint32_t)(pcg_output(s1) >> 32);
-  }
+  r.has_uint32 = (uint32_t)(k & 1);
+  r.uinteger = (uint32_t)(pcg_output(s1) >> 32);  // buffered (odd k) or left stale (even k), as numpy does
   return r;
 }
 
@@ -784,12 +780,8 @@ __device__ void dpu_batched(const Params& P, const TraceDev& T, Shared& S, const
           const U128 s1 = pcg_jump(s0, (unsigned long long)((cnt + 1) >> 1), S.jt);
           c.rng.state_hi = s1.hi;
           c.rng.state_lo = s1.lo;
-          if (cnt & 1) {
-            c.rng.has_uint32 = 1;
-            c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);
-          } else {
-            c.rng.has_uint32 = 0;
-          }
+          c.rng.has_uint32 = (uint32_t)(cnt & 1);
+          c.rng.uinteger = (uint32_t)(pcg_output(s1) >> 32);  // numpy leaves it stale when consumed
         }
       }
     }

@@ -43,6 +43,7 @@
 #include "cache_model.cuh"
 #include "dpu.cuh"
 #include "engine_state.cuh"
+#include "radix_sort.cuh"
 #include "shard.cuh"
 
 namespace rsd {
@@ -121,55 +122,41 @@ __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_fir
   }
 }
 
-// Parity mode: the whole waiting queue of this iteration sorted by (priority
-// bits, rank) -- the reference's (priority, arrival, rel_id) order,
-// engine.py:175-176, 277-281 -- into order row `row` (all threads; a bitonic
-// sort in shared memory).  Never on the timed path: the engine itself only
-// needs the head and the length.
-__device__ __noinline__ void record_waiting_order(const TraceDev& T, Shared& S, long long row) {
-  Ctl& c = S.c;
-  const RqView rq = S.rq;
-  const int tid = threadIdx.x;
-  int n = 0;
-  for (int a0 = 0; a0 < c.n_admitted; a0 += kThreads) {
-    const int a = a0 + tid;
-    const bool w = a < c.n_admitted && rq.q[a] < rq.off[a + 1] - rq.off[a];
-    int v[1] = {w ? 1 : 0}, tot[1];
-    block_scan32<1>(v, S.s32, tot);
-    if (w) {
-      S.ord.key[n + v[0] - 1] = okey(rq.prio[a]);
-      S.ord.rank[n + v[0] - 1] = a;
+// Parity mode: snapshot of this iteration's priority update into row `row`
+// (all threads): every admitted relQuery's priority and flags (estimated /
+// starvation override / live / waiting) and the DPU generator state -- the
+// reference's PriorityRecord per live relQuery (priority.py:287-315) and the
+// generator state after update().  The waiting order (engine.py:277-281) is
+// derived from it after the launch by the radix sort (rs_engine_read_order):
+// the timed path never sorts.
+__device__ __noinline__ void record_parity(const Params& P, const TraceDev& T, Shared& S, long long row) {
+  const Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const rs_config& cfg = P.cfg;
+  double* vp = T.snap_prio + (size_t)row * T.R;
+  unsigned char* fp = T.snap_flag + (size_t)row * T.R;
+  const bool dpu = P.use_dpu;
+  const bool tau_on = dpu && isfinite(cfg.tau);
+  for (int a = threadIdx.x; a < T.R; a += kThreads) {
+    unsigned char f = 0;
+    double v = qnan();
+    if (a < c.n_admitted) {
+      const int size = rq.off[a + 1] - rq.off[a];
+      v = rq.prio[a];
+      if (rq.ndone[a] < size || size == 0) f |= kSnapLive;
+      if (rq.q[a] < size) f |= kSnapWaiting;
+      if (dpu && a >= S.new_lo && a < S.new_hi) f |= kSnapEstimated;  // first sight
+      if (tau_on && rq.q[a] == 0 && size > 0 &&
+          __ddiv_rn(__dsub_rn(c.clock, rq.arrival[a]), (double)size) > cfg.tau)
+        f |= kSnapOverride;
     }
-    n += tot[0];
-  }
-  int n2 = 1;
-  while (n2 < n) n2 <<= 1;
-  for (int i = n + tid; i < n2; i += kThreads) {
-    S.ord.key[i] = ~0ULL;
-    S.ord.rank[i] = 0x7FFFFFFF;
+    vp[a] = v;
+    fp[a] = f;
   }
   __syncthreads();
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < n2; i += kThreads) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long ki = S.ord.key[i], kl = S.ord.key[l];
-          const int ri = S.ord.rank[i], rl = S.ord.rank[l];
-          const bool gt = ki > kl || (ki == kl && ri > rl);
-          if (gt == ((i & k) == 0)) {
-            S.ord.key[i] = kl;
-            S.ord.key[l] = ki;
-            S.ord.rank[i] = rl;
-            S.ord.rank[l] = ri;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  int* out = T.order_buf + (size_t)row * T.R;
-  for (int i = tid; i < T.R; i += kThreads) out[i] = i < n ? S.ord.rank[i] : -1;
+  if (dpu)  // the re-estimated partially prefilled relQueries (every shard's, in a sharded pool)
+    for (int j = threadIdx.x; j < c.n_act; j += kThreads) fp[c.act[j]] |= kSnapEstimated;
+  if (threadIdx.x == 0) T.snap_rng[row] = c.rng;
   __syncthreads();
 }
 
@@ -185,7 +172,7 @@ __device__ __forceinline__ double world_duration(const Params& P, const TraceDev
 }
 
 // kC: the common configuration, fixed at compile time (a DPU policy, tau = inf,
-// no world-model noise, no waiting-order recording, one shard, decision log on,
+// no world-model noise, one shard, decision log on,
 // the default block size 16 and sample size 8):
 // the checks for everything else leave the iteration's instruction stream.
 template <bool kFast, bool kC>
@@ -382,7 +369,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
       S.head = head_l;  // read by other threads only after later barriers
     }
   }
-  if (!kC && cfg.record_order && T.order_buf) record_waiting_order(T, S, c.n_log & (T.log_cap - 1));
+  // parity mode (any kernel, the common one included: the snapshot is a cold call)
+  if (T.snap_prio) record_parity(P, T, S, c.n_log & (T.log_cap - 1));
   phase_mark(c, 2);
 
   // ---- D: candidates (engine.py:285-308)
@@ -1091,7 +1079,78 @@ int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_by
   return RS_OK;
 }
 
+struct DevBuf {  // scratch freed on every return path
+  std::vector<void*> p;
+  template <typename T>
+  cudaError_t get(T** out, size_t n) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) p.push_back(q);
+    *out = (T*)q;
+    return e;
+  }
+  ~DevBuf() {
+    for (void* q : p) cudaFree(q);
+  }
+};
+
+// keys of the static waiting order: okey(priority) per rank, values = the ranks
+__global__ void static_keys_kernel(const double* prio, int R, unsigned long long* key, int* val) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < R; a += gridDim.x * blockDim.x) {
+    key[a] = okey(prio[a]);
+    val[a] = a;
+  }
+}
+
 }  // namespace
+
+// Stable sort of n (key, value) device pairs by key in place (radix_sort.cuh):
+// one CTA up to kSortOneCta pairs, else the multi-CTA passes.
+static int sort_pairs_dev(unsigned long long* k, int* v, long long n, cudaStream_t st) {
+  if (n <= 1) return RS_OK;
+  DevBuf b;
+  unsigned long long* k1 = nullptr;
+  int* v1 = nullptr;
+  RS_CUDA(b.get(&k1, n));
+  RS_CUDA(b.get(&v1, n));
+  if (n <= kSortOneCta) {
+    sort_pairs_one_cta<<<1, kSortThreads, 0, st>>>(k, v, k1, v1, (int)n);
+    RS_CUDA(cudaGetLastError());
+    RS_CUDA(cudaStreamSynchronize(st));  // the scratch is freed on return
+    return RS_OK;
+  }
+  const long long tiles = (n + kSortTile - 1) / kSortTile;
+  unsigned long long* hist = nullptr;
+  unsigned* th = nullptr;
+  RS_CUDA(b.get(&hist, 8 * 256));
+  RS_CUDA(b.get(&th, 256 * tiles));
+  RS_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(unsigned long long), st));
+  sort_global_hist<<<(unsigned)std::min<long long>(tiles * 4, 148 * 4), kSortThreads, 0, st>>>(k, n, hist);
+  RS_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> hh(8 * 256);
+  RS_CUDA(cudaMemcpyAsync(hh.data(), hist, hh.size() * 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  unsigned long long *sk = k, *dk = k1;
+  int *sv = v, *dv = v1;
+  for (int p = 0; p < 8; ++p) {
+    bool same = false;
+    for (int d = 0; d < 256; ++d) same = same || hh[p * 256 + d] == (unsigned long long)n;
+    if (same) continue;  // the identity pass
+    sort_tile_hist<<<(unsigned)tiles, kSortThreads, 0, st>>>(sk, n, 8 * p, th, (int)tiles);
+    sort_scan<<<1, kSortThreads, 0, st>>>(th, 256 * tiles);
+    sort_tile_scatter<<<(unsigned)tiles, kSortThreads, 0, st>>>(sk, sv, dk, dv, n, 8 * p, th, (int)tiles);
+    RS_CUDA(cudaGetLastError());
+    std::swap(sk, dk);
+    std::swap(sv, dv);
+  }
+  if (sk != k) {
+    RS_CUDA(cudaMemcpyAsync(k, sk, n * 8, cudaMemcpyDeviceToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(v, sv, n * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  RS_CUDA(cudaStreamSynchronize(st));
+  return RS_OK;
+}
+
 
 struct rs_engine {
   int device = 0;
@@ -1387,8 +1446,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
       TRY(stage_flush(h));  // the kernel reads the rows and writes fsprio
       first_sight_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d.tok, m, (double*)d.fsprio);
-      cudaError_t ke = cudaGetLastError();
-      if (ke == cudaSuccess) ke = cudaDeviceSynchronize();
+      const cudaError_t ke = cudaGetLastError();  // stream-ordered before the static-order sort below
       if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first_sight_kernel: ") + cudaGetErrorString(ke));
     }
   }
@@ -1416,33 +1474,27 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     }
     hv.off[R] = off[R];
     for (long long i = 0; i < R; ++i) hv.relrank[byid[i]] = (int)i;
-    // static waiting order: a never-prefilled relQuery's priority is its
-    // first-sight estimate (DPU policies), its static priority (sp) or 0 (fcfs)
-    {
-      std::vector<double> zp(R, 0.0);
-      if (cfg->policy == RS_POLICY_SP) {
-        zp = sprio;
-      } else if (dpu && R > 0) {
-        cudaError_t ce = cudaMemcpy(zp.data(), d.fsprio, R * sizeof(double), cudaMemcpyDeviceToHost);
-        if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("first-sight readback: ") + cudaGetErrorString(ce));
-      }
-      std::vector<std::pair<unsigned long long, int>> zk(R);  // (priority bits, rank): stable by the rank
-      for (long long a = 0; a < R; ++a) zk[a] = {okey(zp[a]), (int)a};  // the device's key order
-      std::sort(zk.begin(), zk.end());
-      std::vector<int> z(R);
-      for (long long i = 0; i < R; ++i) z[i] = zk[i].second;
-      h.zorder = z;
-      int nz = 0;  // a shard orders only the relQueries it owns (shard.cuh)
-      for (long long i = 0; i < R; ++i)
-        if (z[i] % shard_world == shard_rank) hv.zl[nz++] = z[i];
-      d.nzl = nz;
-      d.shard_world = shard_world;
-      d.shard_rank = shard_rank;
-    }
+    // static waiting order (rq.zl): a never-prefilled relQuery's priority is its
+    // first-sight estimate (DPU policies), its static priority (sp) or 0 (fcfs),
+    // ordered by (okey(priority), rank) -- the device radix sort at the end of
+    // this function (fcfs: every key is 0, the order is the ranks)
+    for (long long a = 0; a < R; ++a) hv.zl[a] = (int)a;
+    d.nzl = (int)R;
+    d.shard_world = shard_world;
+    d.shard_rank = shard_rank;
     TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size(), h.rq_host.data()));
     h.off.assign(off.begin(), off.end());
   }
   pc.mark("relQuery table");
+  // static-order sort scratch (keys, their ping-pong copies, values' ping-pong copy)
+  const bool zsort = R > 1 && R <= kSortOneCta && (dpu || cfg->policy == RS_POLICY_SP);
+  unsigned long long *zk0 = nullptr, *zk1 = nullptr;
+  int* zv1 = nullptr;
+  if (zsort) {
+    TRY(dalloc(h, &zk0, R));
+    TRY(dalloc(h, &zk1, R));
+    TRY(dalloc(h, &zv1, R));
+  }
   d.fifo_cap = 1;  // >= capacity + kMaxRun + 2: batched pushes precede evictions
   while (d.fifo_cap < cfg->capacity_blocks + kMaxRun + 2) d.fifo_cap <<= 1;
   TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
@@ -1458,9 +1510,11 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     d.log_cap = 1;
     while (d.log_cap < log_cap) d.log_cap <<= 1;
     TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
-    if (cfg->record_order) {  // parity mode (outside the arena: it can be large)
-      if (R > kOrderMax) return fail(RS_EUNSUPPORTED, "record_order supports at most 4096 relQueries");
-      TRY(dalloc(h, &d.order_buf, (size_t)d.log_cap * std::max<long long>(R, 1), nullptr, 0xFF));
+    if (cfg->record_order) {  // parity mode snapshots (outside the arena: they can be large)
+      const size_t cells = (size_t)d.log_cap * std::max<long long>(R, 1);
+      TRY(dalloc(h, &d.snap_prio, cells, nullptr, 0xFF));
+      TRY(dalloc(h, &d.snap_flag, cells, nullptr, 0));
+      TRY(dalloc(h, &d.snap_rng, d.log_cap, nullptr, 0));
     }
   }
   pc.mark("fifo/jump/log");
@@ -1474,8 +1528,50 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   rc = stage_flush(h);
   h.staging = false;
   std::vector<unsigned char>().swap(h.stage);
+  if (rc) return rc;
+  pc.mark("uploads");
+  // the static waiting order on the device: keys from the first-sight
+  // priorities (or sp's static ones in the uploaded table), sorted stably in
+  // place into the table's zl section (radix_sort.cuh); stream-ordered after
+  // the first-sight kernel and the uploads, no host round trip
+  {
+    const RqView dv = rq_carve(d.rq_global, (int)R);
+    if (zsort) {
+      const double* src = dpu ? d.fsprio : dv.prio;
+      static_keys_kernel<<<(unsigned)std::min<long long>((R + 255) / 256, 148 * 8), 256>>>(src, (int)R, zk0, dv.zl);
+      sort_pairs_one_cta<<<1, kSortThreads>>>(zk0, dv.zl, zk1, zv1, (int)R);
+      const cudaError_t ke = cudaGetLastError();
+      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("static order sort: ") + cudaGetErrorString(ke));
+    } else if (R > kSortOneCta && (dpu || cfg->policy == RS_POLICY_SP)) {  // the multi-CTA passes (synchronous)
+      DevBuf b;
+      unsigned long long* k = nullptr;
+      if (b.get(&k, R) != cudaSuccess) return fail(RS_ENOMEM, "static order keys");
+      static_keys_kernel<<<(unsigned)std::min<long long>((R + 255) / 256, 148 * 8), 256>>>(
+          dpu ? d.fsprio : dv.prio, (int)R, k, dv.zl);
+      if ((rc = sort_pairs_dev(k, dv.zl, R, 0))) return rc;
+    }
+    if (shard_world > 1) {
+      // the full order on the host: a shard keeps the relQueries it owns (shard.cuh),
+      // and replicas of this trace on the same device are built from it (clone_replica)
+      h.zorder.assign(R, 0);
+      if (R) {
+        const cudaError_t ce = cudaMemcpy(h.zorder.data(), dv.zl, R * sizeof(int), cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("static order readback: ") + cudaGetErrorString(ce));
+      }
+    }
+    RqView hv = rq_carve(h.rq_host.data(), (int)R);
+    int nz = 0;
+    for (long long i = 0; i < (long long)h.zorder.size(); ++i)
+      if (h.zorder[i] % shard_world == shard_rank) hv.zl[nz++] = h.zorder[i];
+    if (shard_world > 1) {
+      d.nzl = nz;
+      const cudaError_t ce = cudaMemcpy(dv.zl, hv.zl, (size_t)nz * sizeof(int), cudaMemcpyHostToDevice);
+      if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("shard static order: ") + cudaGetErrorString(ce));
+    }
+  }
+  pc.mark("static order");
 #undef TRY
-  return rc;
+  return RS_OK;
 }
 
 // Another shard's replica of a built trace (sharded pool, all shards in one
@@ -1626,7 +1722,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   e->fast = true;
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;
   // the common configuration's specialised kernel (see iterate)
-  e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && !cfg->record_order &&
+  e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) &&
               shard_world == 1 && cfg->log_decisions && cfg->block_size == 16 && cfg->sample_size == 8;
   for (auto& h : e->traces) e->common = e->common && h.dev.log_cap > 0;
   cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
@@ -1793,21 +1889,139 @@ int rs_engine_read_log(rs_engine* e, int32_t t, int64_t first, int64_t count, rs
   return RS_OK;
 }
 
-int rs_engine_read_order(rs_engine* e, int32_t t, int64_t first, int64_t count, int32_t* out) {
+// Parity-mode readers.  Row i of every output is the snapshot of iteration
+// first + i (the ring must still hold it: count <= log capacity, read before
+// the next launch).
+static int parity_rows(rs_engine* e, int32_t t, int64_t first, int64_t count, const HostTrace** hp) {
   if (!e || t < 0 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
   const HostTrace& h = e->traces[t];
+  if (!h.dev.snap_prio) return fail(RS_EINVAL, "engine created without record_order (parity mode)");
+  if (count < 0 || count > h.dev.log_cap) return fail(RS_EINVAL, "range exceeds the parity ring");
+  *hp = &h;
+  return RS_OK;
+}
+
+int rs_engine_read_dpu(rs_engine* e, int32_t t, int64_t first, int64_t count, double* values, uint8_t* flags,
+                       rs_pcg64_state* rng) {
+  const HostTrace* hp = nullptr;
+  int rc = parity_rows(e, t, first, count, &hp);
+  if (rc) return rc;
+  const HostTrace& h = *hp;
   const TraceDev& d = h.dev;
-  if (!d.order_buf) return fail(RS_EINVAL, "engine created without record_order");
-  if (count <= 0) return RS_OK;
-  if (count > d.log_cap) return fail(RS_EINVAL, "order range exceeds the ring buffer");
-  RS_CUDA(cudaSetDevice(e->device));
   const long long R = d.R;
+  RS_CUDA(cudaSetDevice(e->device));
+  std::vector<double> vb(R);
+  std::vector<unsigned char> fb(R);
   for (long long i = 0; i < count; ++i) {
     const long long row = (first + i) & (d.log_cap - 1);
-    RS_CUDA(cudaMemcpy(out + i * R, d.order_buf + row * R, R * sizeof(int), cudaMemcpyDeviceToHost));
-    for (long long k = 0; k < R; ++k)
-      if (out[i * R + k] >= 0) out[i * R + k] = h.order[out[i * R + k]];
+    if (values || flags) {
+      RS_CUDA(cudaMemcpy(vb.data(), d.snap_prio + row * R, R * sizeof(double), cudaMemcpyDeviceToHost));
+      RS_CUDA(cudaMemcpy(fb.data(), d.snap_flag + row * R, R, cudaMemcpyDeviceToHost));
+      for (long long a = 0; a < R; ++a) {  // ranks -> trace order
+        if (values) values[i * R + h.order[a]] = vb[a];
+        if (flags) flags[i * R + h.order[a]] = fb[a];
+      }
+    }
+    if (rng) RS_CUDA(cudaMemcpy(rng + i, d.snap_rng + row, sizeof(rs_pcg64_state), cudaMemcpyDeviceToHost));
   }
+  return RS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// per parity row: the number of waiting relQueries (pass 1) / their (key, rank) at off[i] (pass 2)
+__global__ void __launch_bounds__(kThreads) parity_gather_kernel(const double* snap_prio, const unsigned char* snap_flag,
+                                                                 long long R, long long first, long long mask,
+                                                                 const long long* off, int* cnt,
+                                                                 unsigned long long* key, int* idx, int* rank,
+                                                                 unsigned long long* rowk) {
+  __shared__ Scan32Smem s32;
+  const long long row = (first + blockIdx.x) & mask;
+  const unsigned char* f = snap_flag + row * R;
+  const double* v = snap_prio + row * R;
+  long long base = off ? off[blockIdx.x] : 0;
+  int n = 0;
+  for (long long a0 = 0; a0 < R; a0 += kThreads) {
+    const long long a = a0 + threadIdx.x;
+    const bool w = a < R && (f[a] & kSnapWaiting);
+    int x[1] = {w ? 1 : 0}, tot[1];
+    block_scan32<1>(x, s32, tot);
+    if (off && w) {
+      const long long e = base + n + x[0] - 1;
+      key[e] = okey(v[a]);
+      idx[e] = (int)e;
+      rank[e] = (int)a;
+      rowk[e] = (unsigned long long)blockIdx.x;
+    }
+    n += tot[0];
+  }
+  if (!off && threadIdx.x == 0) cnt[blockIdx.x] = n;
+}
+
+__global__ void parity_rowkeys_kernel(const unsigned long long* rowk, const int* idx, unsigned long long* key2,
+                                      long long n) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    key2[j] = rowk[idx[j]];
+}
+
+__global__ void parity_ranks_kernel(const int* rank, const int* idx, int* out, long long n) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    out[j] = rank[idx[j]];
+}
+
+}  // namespace
+
+extern "C" {
+
+int rs_engine_read_order(rs_engine* e, int32_t t, int64_t first, int64_t count, int32_t* out) {
+  const HostTrace* hp = nullptr;
+  int rc = parity_rows(e, t, first, count, &hp);
+  if (rc) return rc;
+  if (count == 0) return RS_OK;
+  const HostTrace& h = *hp;
+  const TraceDev& d = h.dev;
+  const long long R = d.R;
+  RS_CUDA(cudaSetDevice(e->device));
+  for (long long i = 0; i < count * R; ++i) out[i] = -1;
+  if (R == 0) return RS_OK;
+  DevBuf b;
+  int* cnt = nullptr;
+  long long* off = nullptr;
+  RS_CUDA(b.get(&cnt, count));
+  RS_CUDA(b.get(&off, count + 1));
+  parity_gather_kernel<<<(unsigned)count, kThreads>>>(d.snap_prio, d.snap_flag, R, first, d.log_cap - 1, nullptr, cnt,
+                                                      nullptr, nullptr, nullptr, nullptr);
+  RS_CUDA(cudaGetLastError());
+  std::vector<int> hc(count);
+  RS_CUDA(cudaMemcpy(hc.data(), cnt, count * 4, cudaMemcpyDeviceToHost));
+  std::vector<long long> ho(count + 1, 0);
+  for (long long i = 0; i < count; ++i) ho[i + 1] = ho[i] + hc[i];
+  const long long n = ho[count];
+  if (n == 0) return RS_OK;
+  if (n > 0x7FFFFFF0LL) return fail(RS_EUNSUPPORTED, "parity order read too large; read fewer rows");
+  RS_CUDA(cudaMemcpy(off, ho.data(), (count + 1) * 8, cudaMemcpyHostToDevice));
+  unsigned long long *key = nullptr, *rowk = nullptr;
+  int *idx = nullptr, *rank = nullptr, *res = nullptr;
+  RS_CUDA(b.get(&key, n));
+  RS_CUDA(b.get(&rowk, n));
+  RS_CUDA(b.get(&idx, n));
+  RS_CUDA(b.get(&rank, n));
+  RS_CUDA(b.get(&res, n));
+  parity_gather_kernel<<<(unsigned)count, kThreads>>>(d.snap_prio, d.snap_flag, R, first, d.log_cap - 1, off, cnt, key,
+                                                      idx, rank, rowk);
+  RS_CUDA(cudaGetLastError());
+  // (priority key, rank) order within each row: stable by key from rank order, then stable by row
+  if ((rc = sort_pairs_dev(key, idx, n, 0))) return rc;
+  parity_rowkeys_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256>>>(rowk, idx, key, n);
+  if ((rc = sort_pairs_dev(key, idx, n, 0))) return rc;
+  parity_ranks_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256>>>(rank, idx, res, n);
+  RS_CUDA(cudaGetLastError());
+  std::vector<int> hr(n);
+  RS_CUDA(cudaMemcpy(hr.data(), res, n * 4, cudaMemcpyDeviceToHost));
+  for (long long i = 0; i < count; ++i)
+    for (long long j = ho[i]; j < ho[i + 1]; ++j) out[i * R + (j - ho[i])] = h.order[hr[j]];
   return RS_OK;
 }
 
@@ -2059,6 +2273,26 @@ int rs_choice_sequence(rs_pcg64_state* rng, int64_t n_calls, const int64_t* n, c
   cudaFree(d_n);
   cudaFree(d_k);
   cudaFree(d_out);
+  return RS_OK;
+}
+
+int rs_sort_pairs(const uint64_t* keys, const int32_t* values, int64_t n, uint64_t* keys_out, int32_t* values_out,
+                  int32_t device) {
+  if (n < 0 || (n && (!keys || !values || !keys_out || !values_out))) return fail(RS_EINVAL, "bad sort input");
+  if (n > 0x7FFFFFF0LL) return fail(RS_EINVAL, "too many pairs");
+  RS_CUDA(cudaSetDevice(device));
+  if (n == 0) return RS_OK;
+  DevBuf b;
+  unsigned long long* k = nullptr;
+  int* v = nullptr;
+  RS_CUDA(b.get(&k, n));
+  RS_CUDA(b.get(&v, n));
+  RS_CUDA(cudaMemcpy(k, keys, n * 8, cudaMemcpyHostToDevice));
+  RS_CUDA(cudaMemcpy(v, values, n * 4, cudaMemcpyHostToDevice));
+  const int rc = sort_pairs_dev(k, v, n, 0);
+  if (rc) return rc;
+  RS_CUDA(cudaMemcpy(keys_out, k, n * 8, cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(values_out, v, n * 4, cudaMemcpyDeviceToHost));
   return RS_OK;
 }
 

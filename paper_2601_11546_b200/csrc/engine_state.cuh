@@ -33,7 +33,6 @@ constexpr int kEstBatch = 128;  // relQueries re-estimated per DPU batch
 constexpr int kDrawBuf = 4096;  // numpy next32 draws staged per DPU batch
 constexpr int kItemBuf = 2048;  // PEM items staged per segment-parallel batch
 constexpr int kPhases = 24;
-constexpr int kOrderMax = 4096;  // parity mode: relQueries whose full waiting order is recorded
 constexpr int kSmallEst = 32;   // DPU fast path: at most this many re-estimated relQueries
 constexpr int kSmallMns = 256;  // ... and max_num_seqs at most this
 constexpr int kMaxJobs = 64;    // ... and at most this many PEM segments
@@ -131,6 +130,12 @@ __host__ __device__ inline RqView rq_carve(void* base, int R) {
   return v;
 }
 
+// parity-mode snapshot flags per relQuery and iteration (rs_engine_read_dpu)
+constexpr unsigned char kSnapEstimated = 1;  // priority recomputed this iteration (not reused, priority.py:296-303)
+constexpr unsigned char kSnapOverride = 2;   // starvation override applied (priority.py:318-339)
+constexpr unsigned char kSnapLive = 4;       // in live_relqueries (admitted, not retired; engine.py:254, 362)
+constexpr unsigned char kSnapWaiting = 8;    // has pending (unprefilled) rows: in the waiting queue (engine.py:280)
+
 struct TraceDev {
   int R, N, max_size, seg_ok;  // seg_ok: mns * max(tok) <= cap (PEM segments close by count only)
   int rq_in_smem, pad0;
@@ -159,7 +164,10 @@ struct TraceDev {
   long long noise_n;         // ... available (rs_engine_set_noise)
   rs_iter_record* log;
   long long log_cap;
-  int* order_buf;  // parity mode: [log_cap][R] waiting order per logged iteration (ranks)
+  // parity mode (cfg.record_order), per logged iteration (row = n_log & (log_cap - 1)):
+  double* snap_prio;            // [log_cap][R] every admitted relQuery's priority after the update (NaN: not admitted)
+  unsigned char* snap_flag;     // [log_cap][R] kSnap* bits
+  rs_pcg64_state* snap_rng;     // [log_cap] the DPU generator after the update
   Ctl* ctl;
 };
 
@@ -233,10 +241,6 @@ struct Shared {
       int nterm[kMaxJobs];
       int U[kWarps][kSmallMns];  // per-warp utok prefix of the segment it evaluates
     } small;
-    struct {  // parity mode: the waiting queue being sorted
-      unsigned long long key[kOrderMax];
-      int rank[kOrderMax];
-    } ord;
     struct {
       unsigned long long t0[kWin];
       unsigned long long c0[kWin];

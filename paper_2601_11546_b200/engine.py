@@ -82,6 +82,12 @@ class RunResult:
     #: parity mode (Engine(record_waiting_order=True)): per iteration, the waiting queue after the
     #: priority update as trace-order relQuery indices (engine.py:277-281)
     waiting_orders: list | None = None
+    #: parity mode, DPU policies: per iteration, DynamicPriorityUpdater.update's records
+    #: (priority.py:287-315) in live-relQuery order -- PriorityRecords(rel_id, value, reused,
+    #: starvation_override), numpy columns -- and the DPU generator state after the update
+    #: ((state, has_uint32, uinteger), numpy's bit_generator.state fields)
+    priority_records: list | None = None
+    dpu_rng_states: list | None = None
 
     @property
     def cache_hit_ratio(self) -> float:
@@ -120,6 +126,17 @@ class RunResult:
             for e in self.decision_log:
                 w.writerow([e.iteration, repr(e.clock), e.case, e.m_plus, e.m_minus,
                             e.delta_plus, e.delta_minus, e.delta_total, e.action])
+
+
+@dataclass
+class PriorityRecords:
+    """One iteration's DPU records as columns (priority.py:62-68), live relQueries in
+    admission order (the reference's dict order)."""
+
+    rel_id: np.ndarray
+    value: np.ndarray
+    reused: np.ndarray
+    starvation_override: np.ndarray
 
 
 @dataclass
@@ -282,8 +299,10 @@ class Engine:
         """shards > 1 runs the sharded pool (include/relserve.h rs_engine_create_sharded):
         shard_rank -1 puts every shard on `device` (one CTA each); shard_rank >= 0 makes this
         engine one shard of a multi-process group (call connect_shards before run/step).
-        record_waiting_order (parity mode): also record the full sorted waiting queue of every
-        iteration (RunResult.waiting_orders); the timed path never sorts."""
+        record_waiting_order (parity mode): also record, for every iteration, the priority
+        update (RunResult.priority_records, dpu_rng_states) and the full sorted waiting queue
+        (RunResult.waiting_orders, rebuilt from the priorities by the device radix sort); the
+        timed path never sorts."""
         if policy not in POLICIES:
             raise ValueError(f"unknown policy {policy!r}; choose from {POLICIES}")
         self.trace = trace
@@ -303,6 +322,10 @@ class Engine:
 
         self._m = _marshal.marshal_trace(trace, c.block_size, policy, self.policy_model,
                                          c.sp_priority_fns)
+        self._record_order = bool(record_waiting_order and c.log_decisions)
+        if self._record_order:  # parity snapshots: log capacity x relQueries cells, read after each launch
+            R = max(1, trace.columns().num_relqueries)
+            self.chunk_iterations = max(16, min(Engine.chunk_iterations, 1 << max(4, ((1 << 24) // R).bit_length() - 1)))
         self._native = _native.NativeEngine(
             [self._m.view], _marshal.make_config(c, policy, record_waiting_order and c.log_decisions),
             _marshal.make_model(world_model),
@@ -310,8 +333,8 @@ class Engine:
             log_capacity=self.chunk_iterations if c.log_decisions else 0, shards=shards, rank=shard_rank,
         )
         self.shards, self.shard_rank = shards, shard_rank
-        self._record_order = bool(record_waiting_order and c.log_decisions)
         self._orders: list[np.ndarray] = []
+        self._dpu_snaps: list = []
         # world-model noise (engine.py:198, 310-313): the reference's standard normals, one per
         # executed batch, from the same stream; handed to the device in growing prefixes
         self._noise_rng = None
@@ -372,8 +395,9 @@ class Engine:
         if self.config.log_decisions and st.n_log > self._n_read:
             self._records.append(self._native.read_log(0, self._n_read, st.n_log - self._n_read))
             if self._record_order:
-                self._orders.append(self._native.read_order(0, self._n_read, st.n_log - self._n_read,
-                                                            self.trace.columns().num_relqueries))
+                R = self.trace.columns().num_relqueries
+                self._orders.append(self._native.read_order(0, self._n_read, st.n_log - self._n_read, R))
+                self._dpu_snaps.append(self._native.read_dpu(0, self._n_read, st.n_log - self._n_read, R))
             self._n_read = st.n_log
 
     def run(self) -> RunResult:
@@ -429,7 +453,26 @@ class Engine:
             cache_hit_tokens=int(st.cache_hit_tokens),
             cache_miss_tokens=int(st.cache_miss_tokens), completion_iteration=comp, records=recs,
             device_wall_s=wall, waiting_orders=self._waiting_orders(recs),
+            **self._priority_records(),
         )
+
+    def _priority_records(self) -> dict:
+        if not self._record_order or self.policy in ("fcfs", "sp"):  # no DPU (engine.py:221-227)
+            return {}
+        c = self.trace.columns()
+        adm = np.lexsort((c.rel_id, c.arrival))  # live_relqueries order (engine.py:211-213, 254)
+        rid = c.rel_id[adm]
+        recs, rngs = [], []
+        for vals, flags, rng in self._dpu_snaps:
+            v, f = vals[:, adm], flags[:, adm]
+            for i in range(len(v)):
+                live = (f[i] & _abi.SNAP_LIVE) != 0
+                fi = f[i][live]
+                recs.append(PriorityRecords(rid[live], v[i][live], (fi & _abi.SNAP_ESTIMATED) == 0,
+                                            (fi & _abi.SNAP_OVERRIDE) != 0))
+            for r in rng:
+                rngs.append(((r.state_hi << 64) | r.state_lo, int(r.has_uint32), int(r.uinteger)))
+        return {"priority_records": recs, "dpu_rng_states": rngs}
 
     def _waiting_orders(self, recs):
         if not self._record_order:

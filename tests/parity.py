@@ -139,3 +139,28 @@ def golden_dpu_by_iter(g):
         if "dpu" in e:
             out[e["it"]] = {rid: val for rid, val, reused, ov in e["dpu"] if not reused}
     return out
+
+
+def compare_priority_records(res, g, what: str = "run") -> int:
+    """Device DPU records (RunResult.priority_records, parity mode) against the golden's
+    `dpu` rows (priority.py:287-315: value, reused, starvation_override per live relQuery in
+    dict order; only the recomputed ones in fixtures recorded with full=False) and the DPU
+    generator state after each update.  Values compare bit for bit.  Returns the iterations
+    checked."""
+    n = 0
+    for i, e in enumerate(g["iters"]):
+        if "dpu" not in e:
+            continue
+        pr = res.priority_records[i]
+        full = any(row[2] for row in e["dpu"]) or len(e["dpu"]) == len(pr.rel_id)
+        rows = [[int(r), float(v), int(u), int(o)] for r, v, u, o in
+                zip(pr.rel_id.tolist(), pr.value.tolist(), pr.reused.tolist(), pr.starvation_override.tolist())]
+        if not full:
+            rows = [[r, v, 0, o] for r, v, u, o in rows if not u]
+        want = [[int(r), float(v), int(u), int(o)] for r, v, u, o in e["dpu"]]
+        assert rows == want, f"{what}: DPU records differ at iteration {e['it']}: " + next(
+            (f"{a} != {b}" for a, b in zip(rows, want) if a != b), f"{len(rows)} vs {len(want)} records")
+        st, has, u = res.dpu_rng_states[i]
+        assert [str(st), has, u] == e["rng"], f"{what}: DPU RNG state differs at iteration {e['it']}"
+        n += 1
+    return n

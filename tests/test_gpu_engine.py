@@ -108,13 +108,13 @@ def test_noise_prefix_refill_matches_reference_golden(chunk, monkeypatch):
     assert res.sim_duration == g["result"]["sim_duration"]
 
 
-ORDER_GOLDENS = [n for n in golden_names() if any("order" in e for e in load_golden(n)["iters"][:3])]
-
-
-@pytest.mark.parametrize("name", ORDER_GOLDENS)
-def test_device_full_waiting_order_matches_reference(name):
-    """Parity mode: the whole waiting queue (engine.py:277-281, sorted by (priority,
-    arrival, rel_id)) of every iteration equals the reference's, entry for entry."""
+@pytest.mark.parametrize("name", golden_names())
+def test_device_parity_mode_matches_reference(name):
+    """Parity mode on every golden: the priority update of every iteration (each live
+    relQuery's value, reused and override flags, priority.py:287-315, and the DPU generator
+    state after it) and -- where the golden recorded it -- the whole waiting queue
+    (engine.py:277-281, sorted by (priority, arrival, rel_id); rebuilt from the priorities by
+    the device radix sort) equal the reference's, bit for bit, along with every decision."""
     from paper_2601_11546_b200.engine import Engine, SimulationAborted
 
     g = load_golden(name)
@@ -125,6 +125,7 @@ def test_device_full_waiting_order_matches_reference(name):
     except SimulationAborted:
         res = eng.result
     eng.close()
+    parity.compare_records(res.records, g, trace, f"parity/{name}")
     rel = trace.columns().rel_id
     n = 0
     for e in g["iters"]:
@@ -132,7 +133,11 @@ def test_device_full_waiting_order_matches_reference(name):
             got = [int(rel[i]) for i in res.waiting_orders[e["it"]]]
             assert got == e["order"], f"{name}: waiting order differs at iteration {e['it']}"
             n += 1
-    assert n > 0
+        assert len(res.waiting_orders[e["it"]]) == e["W"]
+    if policy in ("fcfs", "sp"):
+        assert res.priority_records is None
+    else:
+        assert parity.compare_priority_records(res, g, name) == len(g["iters"])
 
 
 def test_pinned_trace_and_result_readback():

@@ -2,7 +2,10 @@
 capacities, sample sizes (fast path and general DPU path), starvation
 thresholds, world-model noise and shard counts, each run on the device and on the CPU oracle
 and compared bit for bit (decisions, Delta terms, waiting head/count, batches,
-kv, clock, completion iterations, ledgers, cache counters)."""
+kv, clock, completion iterations, ledgers, cache counters).  The device runs in
+parity mode, so every iteration's priority records (value, reused, override of
+each live relQuery), DPU generator state and whole waiting queue are compared
+with the oracle's too."""
 
 import math
 
@@ -42,13 +45,14 @@ def test_random_sweep_device_equals_oracle(i, oracle_mod):
     trace = generate_trace(TraceConfig(**tc))
     cfg = EngineConfig(constraints=SchedulerConstraints(*cons), iteration_limit=20_000, **kw)
     w = world_preset(model)
-    ref = oracle_mod.run(trace, policy, w, cfg, None, seed)
+    O = oracle_mod
+    ref = O.run(trace, policy, w, cfg, None, seed, record=O.OR_REC_DPU | O.OR_REC_WAITING | O.OR_REC_RNG)
     if ref.status == 2:  # a request does not fit the tight cap: both sides must refuse
         with pytest.raises(InfeasibleRequestError):
             Engine(trace, policy, w, cfg, None, seed, device=0)
         return
     try:
-        eng = Engine(trace, policy, w, cfg, None, seed, device=0, shards=shards)
+        eng = Engine(trace, policy, w, cfg, None, seed, device=0, shards=shards, record_waiting_order=True)
     except NotImplementedError as e:  # outside the device model (documented): e.g. truncated cache inserts
         pytest.skip(str(e))
     try:
@@ -67,3 +71,20 @@ def test_random_sweep_device_equals_oracle(i, oracle_mod):
         assert np.array_equal(a, b, equal_nan=a.dtype.kind == "f"), k
     assert np.array_equal(res.completion_iteration, ref.completion_iter)
     assert (res.cache_hit_tokens, res.cache_miss_tokens) == (ref.cache_hit_tokens, ref.cache_miss_tokens)
+    n = len(ref.log)
+    rel = trace.columns().rel_id
+    for it in range(n):
+        lo, hi = ref.wait_off[it], ref.wait_off[it + 1]
+        assert np.array_equal(res.waiting_orders[it], ref.wait[lo:hi]), f"waiting order, iteration {it}"
+    if policy in ("fcfs", "sp") or ref.dpu is None:
+        return
+    for it in range(n):
+        d = ref.dpu[ref.dpu_off[it]:ref.dpu_off[it + 1]]
+        pr = res.priority_records[it]
+        assert np.array_equal(pr.rel_id, rel[d["rq"]]), f"live relQueries, iteration {it}"
+        assert np.array_equal(pr.value.view(np.uint64), d["value"].view(np.uint64)), f"priorities, iteration {it}"
+        assert np.array_equal(pr.reused, d["reused"] != 0), f"reused flags, iteration {it}"
+        assert np.array_equal(pr.starvation_override, d["overridden"] != 0), f"override flags, iteration {it}"
+        st, has, u = res.dpu_rng_states[it]
+        assert (st, has, u) == ((int(ref.rng_trace[it, 0]) << 64) | int(ref.rng_trace[it, 1]),
+                                int(ref.rng_trace[it, 2]), int(ref.rng_trace[it, 3])), f"RNG, iteration {it}"

@@ -60,7 +60,7 @@ def test_waiting_argmin_matches_reference_sort():
 
     r = np.random.default_rng(5)
     for n in (0, 1, 7, 512, 513, 5000, 70_000):
-        prio = r.choice([0.0, 0.25, 1.5, 3.0], n) if n % 2 else r.uniform(0, 10, n)
+        prio = r.choice([0.0, 0.25, 1.5, 3.0, -0.5, -4.0], n) if n % 2 else r.uniform(-10, 10, n)
         wait = r.random(n) < 0.6
         head, count = waiting_argmin(prio, wait)
         ranks = np.flatnonzero(wait)
@@ -70,8 +70,10 @@ def test_waiting_argmin_matches_reference_sort():
             continue
         # admission order is (arrival, rel_id), so rank order breaks priority ties
         assert head == ranks[np.lexsort((ranks, prio[ranks]))[0]]
-    with pytest.raises(ValueError):
-        waiting_argmin(np.array([1.0, -2.0]), np.array([1, 1]))
+    assert waiting_argmin(np.array([1.0, -2.0]), np.array([1, 1])) == (1, 2)  # sp priorities may be negative
+    for bad in (np.nan, -0.0):
+        with pytest.raises(ValueError):
+            waiting_argmin(np.array([1.0, bad]), np.array([1, 1]))
 
 
 def test_pem_reference_tests():
@@ -88,3 +90,25 @@ def test_pem_reference_tests():
     assert hi >= lo
     full = pem([RemainderItem(None, 80, 4, False)] * 6, c, model)
     assert pem([RemainderItem(None, 80, 4, False)] * 5, c, model) <= full
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 1000, 65536, 65537, 300_000])
+def test_radix_sort_is_a_stable_sort(n):
+    """North-star kernel 2 (rs_sort_pairs): equals numpy's stable argsort, duplicates
+    keeping their input order; keys built like the engine's (okey of priorities of
+    either sign, many ties)."""
+    rs = np.random.default_rng(n)
+    prio = rs.choice(np.concatenate([rs.normal(0, 50, 64), [0.0, 1.5, -2.25]]), size=n)
+    keys = _native.priority_keys(prio)
+    if n > 2:
+        keys[: n // 3] = rs.integers(0, 2**63, size=n // 3, dtype=np.uint64) * np.uint64(2)  # full-width keys too
+    vals = np.arange(n, dtype=np.int32)
+    ko, vo = _native.sort_pairs(keys, vals)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(vo, vals[order]) and np.array_equal(ko, keys[order])
+
+
+def test_priority_keys_order_numbers():
+    x = np.array([-np.inf, -1e300, -2.5, -1.0, -5e-324, 0.0, 5e-324, 1.0, 2.5, 1e300, np.inf])
+    k = _native.priority_keys(x)
+    assert np.all(np.diff(k.astype(object)) > 0)

@@ -14,7 +14,7 @@ def test_oracle_matches_reference_golden(name, oracle_mod):
     O = oracle_mod
     g = load_golden(name)
     trace, policy, world, cfg, pm, seed = parity.golden_inputs(g)
-    res = O.run(trace, policy, world, cfg, pm, seed, record=O.OR_REC_DPU | O.OR_REC_WAITING)
+    res = O.run(trace, policy, world, cfg, pm, seed, record=O.OR_REC_DPU | O.OR_REC_WAITING | O.OR_REC_RNG)
     parity.compare_records(res.log, g, trace, f"oracle/{name}")
     parity.compare_completion(res.completion_iter, g, trace)
     parity.compare_ledgers(res.first_prefill_start, res.last_prefill_end, res.last_decode_end, g, trace)
@@ -34,8 +34,11 @@ def test_oracle_matches_reference_golden(name, oracle_mod):
         if "order" in e:
             lo, hi = res.wait_off[e["it"]], res.wait_off[e["it"] + 1]
             assert [int(rel[i]) for i in res.wait[lo:hi]] == e["order"], f"waiting order it {e['it']}"
-        if "rng" in e and res.rng_trace is not None:
-            pass
+        if "rng" in e:  # the DPU generator after update() (numpy bit_generator.state)
+            hi, lo, has, u = (int(x) for x in res.rng_trace[e["it"]])
+            assert [str((hi << 64) | lo), has, u] == e["rng"], f"DPU RNG state differs at iteration {e['it']}"
+    if policy not in ("fcfs", "sp"):
+        assert any("rng" in e for e in g["iters"])
 
 
 def test_goldens_cover_the_scope():
