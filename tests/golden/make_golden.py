@@ -312,10 +312,10 @@ CASES = {
                        policy="fcfs", world=list(TEST_MODEL), config={"noise_sigma": 0.5}, seed=2),
     # configs 2 / 3: windowed (first 40 iterations)
     "cfg2_window": dict(spec=gen({"num_relqueries": 1000, "size_range": [1000, 1000], "rate": 1e6, "seed": 0}),
-                        policy="relserve", world="opt-13b-like", window=40, full=False),
+                        policy="relserve", world="opt-13b-like", window=40),
     "cfg3_window": dict(spec={"kind": "heavy", "config": {"num_relqueries": 5000, "size_range": [1, 399],
                                                            "rate": 1e6, "seed": 0}},
-                        policy="relserve", world="llama-70b-like", window=40, full=False),
+                        policy="relserve", world="llama-70b-like", window=40),
 }
 
 
