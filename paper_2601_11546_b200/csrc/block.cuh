@@ -252,3 +252,74 @@ __device__ __forceinline__ void block_count_argmin(int& cnt, unsigned long long&
 }
 
 }  // namespace rsd
+
+namespace rsd {
+
+// ---------------------------------------------------------------------------
+// Warp groups with their own named barrier (bar.sync id, n): the pipelined
+// common-configuration iteration runs the state advance on warps 0-7 (group
+// M, barrier 1) while warps 8-15 (group D, barrier 2) compute the next
+// iteration's priority update; barrier 0 (__syncthreads) is the whole CTA.
+// ---------------------------------------------------------------------------
+template <int N, int BAR>
+struct Grp {
+  static constexpr int kN = N;
+  static constexpr int kW = N / 32;
+  __device__ __forceinline__ static void sync() {
+    if constexpr (BAR == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(N) : "memory");
+  }
+  // barrier + OR of a predicate over the group
+  __device__ __forceinline__ static bool sync_or(bool p) {
+    if constexpr (BAR == 0) {
+      return __syncthreads_or(p);
+    } else {
+      int r;
+      asm volatile(
+          "{\n\t.reg .pred q, o;\n\t"
+          "setp.ne.s32 q, %1, 0;\n\t"
+          "bar.red.or.pred o, %2, %3, q;\n\t"
+          "selp.s32 %0, 1, 0, o;\n\t}"
+          : "=r"(r)
+          : "r"((int)p), "n"(BAR), "n"(N)
+          : "memory");
+      return r != 0;
+    }
+  }
+};
+using GAll = Grp<kThreads, 0>;
+constexpr int kMWarps = 8;                   // group M: warps [0, 8)
+constexpr int kDWarps = kWarps - kMWarps;    // group D: warps [8, 16)
+using GM = Grp<kMWarps * 32, 1>;
+using GD = Grp<kDWarps * 32, 2>;
+constexpr int kBarHandoff = 3;  // group D has read the state group M is about to change
+
+__device__ __forceinline__ void handoff_arrive() {  // group D
+  asm volatile("bar.arrive %0, %1;" ::"n"(kBarHandoff), "n"(kThreads) : "memory");
+}
+__device__ __forceinline__ void handoff_wait() {  // group M
+  asm volatile("bar.sync %0, %1;" ::"n"(kBarHandoff), "n"(kThreads) : "memory");
+}
+
+// block_scan32 over the G::kN threads of a group (thread index within the group
+// = threadIdx.x - base; the group's warps are consecutive)
+template <class G, int N>
+__device__ __forceinline__ void group_scan32(int (&v)[N], Scan32Smem& sm, int (&tot)[N], int warp_in_group) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < N; ++c) v[c] = warp_incl_scan(v[c]);
+  if (lane == 31) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) sm.w[c][warp_in_group] = v[c];
+  }
+  G::sync();
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    const unsigned x = lane < G::kW ? (unsigned)sm.w[c][lane] : 0u;
+    tot[c] = (int)__reduce_add_sync(kFull, x);
+    v[c] += (int)__reduce_add_sync(kFull, lane < warp_in_group ? x : 0u);
+  }
+  G::sync();
+}
+
+}  // namespace rsd

@@ -201,7 +201,10 @@ __device__ void drain_sequential(Shared& S, const TraceDev& T, long long E, int 
 // in shared memory) and the chain candidates.  Returns false (nothing
 // changed) when the preconditions fail; the caller then runs the exact
 // per-row path.  tokv: the batch rows' tok (staged by the candidate scan).
-template <bool kC>
+// G: the executing warp group (the whole CTA, or group M of the pipelined
+// iteration); kHand: group M waits at the handoff barrier before its first
+// write of state group D reads (rq.m in the drain) -- only when returning true.
+template <bool kC, class G = GAll, bool kHand = false>
 __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int h, int n, const int* tokv,
                              long long& ut_out) {
   Ctl& c = S.c;
@@ -214,22 +217,22 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   const unsigned long long tc = c.tclock;
   const long long head0 = c.fifo_head, tail0 = c.fifo_tail, count0 = c.count;
   // 1. per-row tail blocks: prefix sums of (tail, tok, tail-less rows) in one scan
-  long long Tv[kMaxRun / kThreads], inclT[kMaxRun / kThreads];
+  long long Tv[kMaxRun / G::kN], inclT[kMaxRun / G::kN];
   long long cT = 0, cTok = 0;
   int n_bad = 0;
 #pragma unroll
-  for (int s = 0; s < kMaxRun / kThreads; ++s) {
+  for (int s = 0; s < kMaxRun / G::kN; ++s) {
     Tv[s] = 0;
     inclT[s] = 0;
-    if (s * kThreads < n) {
-      const int i = s * kThreads + tid;
+    if (s * G::kN < n) {
+      const int i = s * G::kN + tid;
       int tk = 0, tl = 0;
       if (i < n) {
         tk = tokv[i];
         tl = (int)(tk / B) - Pc;
       }
       int v[3] = {tl, tk, (i < n && tl <= 0) ? 1 : 0}, tot[3];
-      block_scan32<3>(v, S.s32, tot);
+      group_scan32<G, 3>(v, S.s32, tot, tid >> 5);
       Tv[s] = tl;
       inclT[s] = cT + v[0];
       cT += tot[0];
@@ -245,8 +248,8 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   phase_mark(c, 13);
   // 2. FIFO pushes: row i's chain / tail touch times from prefix sums of touches
 #pragma unroll
-  for (int s = 0; s < kMaxRun / kThreads; ++s) {
-    const int i = s * kThreads + tid;
+  for (int s = 0; s < kMaxRun / G::kN; ++s) {
+    const int i = s * G::kN + tid;
     if (i < n) {
       const long long before =
           i == 0 ? 0 : (long long)m0 + (long long)(i - 1) * Pc + (long long)i * Pc + (inclT[s] - Tv[s]);
@@ -262,7 +265,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   }
   //    stage the FIFO head (the oldest tails) and their relQueries' chain state;
   //    thread 0 meanwhile drops h from the chain candidates (its chain is touched)
-  for (int j = tid; j < Wn; j += kThreads) {
+  for (int j = tid; j < Wn; j += G::kN) {
     const FifoEnt e = T.fifo[(head0 + j) & (T.fifo_cap - 1)];
     S.win.t0[j] = e.t0;
     S.win.rank[j] = e.rank;
@@ -278,8 +281,9 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
     S.fp_par = c.cc_n == 0;
     S.fp_cut = 0x7FFFFFFF;
   }
-  __syncthreads();
+  G::sync();
   phase_mark(c, 14);
+  if constexpr (kHand) handoff_wait();  // group D has read the chain lengths (rq.m) it uses
   // 3. Parallel drain (no chain candidate pending): in LRU order the FIFO units
   // are consumed front to back, each relQuery's chain right after its last
   // tail -- provided that chain is older than the next unit's leaf.  Blocks
@@ -289,7 +293,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   bool par = S.fp_par;
   if (par && E > 0) {
     long long carry = 0;
-    for (int base = 0; base < Wn; base += kThreads) {
+    for (int base = 0; base < Wn; base += G::kN) {
       const int j = base + tid;
       int bj = 0;
       if (j < Wn) {
@@ -299,21 +303,21 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
         bj = S.win.tres[j] + (last ? S.win.mm[j] : 0);
       }
       int v[1] = {bj}, tot[1];
-      block_scan32<1>(v, S.s32, tot);
+      group_scan32<G, 1>(v, S.s32, tot, tid >> 5);
       if (j < Wn && carry + v[0] >= E && carry + v[0] - bj < E) {  // the unique cut unit
         S.fp_cut = j;
         S.fp_rem = E - (carry + v[0] - bj);
       }
       carry += tot[0];
     }
-    __syncthreads();
+    G::sync();
     const int cut = S.fp_cut;
     if (cut == 0x7FFFFFFF) {
       par = false;
     } else {
       const long long rem_cut = S.fp_rem;
       bool bad = false;
-      for (int j = tid; j <= cut && j < Wn; j += kThreads) {
+      for (int j = tid; j <= cut && j < Wn; j += G::kN) {
         const bool chain_evicted = S.win.last[j] && (j < cut || rem_cut > S.win.tres[j]);
         if (chain_evicted) {
           const unsigned long long kc = S.win.c0[j] + (unsigned long long)(S.win.mm[j] - 1);
@@ -322,9 +326,9 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
           if ((!next_in && j + 1 < n_old) || !(kc < kn)) bad = true;
         }
       }
-      par = !__syncthreads_or(bad);
+      par = !G::sync_or(bad);
       if (par) {
-        for (int j = tid; j < cut; j += kThreads) {
+        for (int j = tid; j < cut; j += G::kN) {
           atomicSub(&rq.ntails[S.win.rank[j]], 1);
           if (S.win.last[j]) rq.m[S.win.rank[j]] = 0;
         }
@@ -365,7 +369,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
       }
       drain_sequential(S, T, E, Wn, head0);
     }
-    __syncthreads();
+    G::sync();
   }
   if (tid == 0) {
     const long long hitb = (long long)m0 + (long long)(n - 1) * Pc;
@@ -381,7 +385,7 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
   }
   // 5. reset the staging counters; the sequential drain's popped units lose a tail
   const int popped = par ? 0 : S.fp_popped;
-  for (int j = tid; j < Wn; j += kThreads) {
+  for (int j = tid; j < Wn; j += G::kN) {
     const int a = S.win.rank[j];
     if (j < popped) atomicSub(&rq.ntails[a], 1);
     rq.scr_cnt[a] = 0;

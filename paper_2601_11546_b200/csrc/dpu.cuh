@@ -466,6 +466,371 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
   return n_est;
 }
 
+// Pipelined priority update (engine_kernel<true, true>, warps kMWarps..15 =
+// group D).  While group M executes this iteration's decided action, group D
+// computes the NEXT iteration's re-estimates of the partially prefilled
+// relQueries (the c.act list, priority.py:261-303) from the state that action
+// leaves -- known before it is applied:
+//   prefill of rows [q, q+n) of the head h: q_h += n, h's chain becomes fully
+//     resident (m_h = chain_h: every insert of the batch pins it), the n rows
+//     join the running set with remaining = output_limit, and h joins the list
+//     if this is its first prefill (engine.py:315-341);
+//   decode: every running row's remaining drops by one and finished rows leave
+//     (engine.py:343-363); a relQuery with no unprefilled and no running row
+//     left retires and is not updated;
+//   idle: nothing changes.
+// The sampled ratios use the chain lengths seen now; the prefill advance may
+// evict another relQuery's chain (cache_model.cuh), so spec_commit checks every
+// chain length used against the advance's result.  The numpy draws continue
+// from this iteration's final generator state, in the same list order.  Every
+// input is read before the handoff barrier (group M writes none of them
+// earlier); results go to S.spec_* and are committed after the join.  Only the
+// fast path's shape (<= kSmallEst relQueries, <= kMaxJobs PEM segments, no
+// Lemire rejection) is speculated; otherwise the next iteration runs
+// dpu_update in place.
+__device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const int action, const int h, const int nh,
+                         const bool allowed) {
+  const Ctl& c = S.c;
+  const RqView rq = S.rq;
+  const int lane = threadIdx.x & 31, gw = opaque_warp() - kMWarps;
+  const int dt = threadIdx.x - kMWarps * 32;
+  const bool pf = action == RS_ACTION_PREFILL, dec = action == RS_ACTION_DECODE;
+  const int n_act = c.n_act;
+  const bool join = pf && rq.q[h] == 0;  // h's first prefill: it joins the list
+  const int n_est = n_act + (join ? 1 : 0);
+  if (!allowed || n_est > kSmallEst || n_est == 0) {  // group-uniform
+    if (dt == 0) {
+      S.spec_valid = n_est == 0 && allowed;  // nothing to re-estimate: trivially done
+      S.spec_n = 0;
+      S.spec_rng = c.rng;
+      S.spec_alg = 0;
+    }
+    handoff_arrive();
+    return;
+  }
+  constexpr int Ssz = 8, dper = 2 * Ssz - 1;  // kC: the default sample size (engine.py:150)
+  PemModel pm;
+  pm.ap = P.pol.alpha_p;
+  pm.bp = P.pol.beta_p;
+  pm.ad = P.pol.alpha_d;
+  pm.bd = P.pol.beta_d;
+  pm.cap = P.cfg.cap;
+  pm.mns = P.cfg.max_num_seqs;
+  pm.mnbt = P.cfg.max_num_batched_tokens;
+  // 0. the list and each entry's state after the advance
+  if (gw == 0) {
+    const int x = lane < n_act ? c.act[lane] : 0x7FFFFFFF;
+    const int pos = join ? __popc(__ballot_sync(kFull, x < h)) : 32;
+    const int xm1 = __shfl_up_sync(kFull, x, 1);
+    const int a = lane < pos ? x : (lane == pos ? h : xm1);
+    if (lane < n_est) {
+      const int off = rq.off[a], size = rq.off[a + 1] - off;
+      const bool isH = pf && a == h;
+      const int q = rq.q[a] + (isH ? nh : 0);
+      const int ol = rq.ol[a];
+      S.spec_rank[lane] = a;
+      S.spec_m[lane] = isH ? rq.chain[a] : rq.m[a];
+      S.spec_nunp[lane] = size - q;
+      S.spec_base[lane] = off + q;
+      S.spec_ol[lane] = ol;
+      S.spec_L[lane] = isH ? nh : 0;  // the batch's rows join the running set, remaining = output_limit
+      S.spec_rsum[lane] = isH ? nh * ol : 0;
+      S.spec_rmax[lane] = isH ? ol : 0;
+    }
+    if (lane == 0) {
+      S.spec_n = n_est;
+      S.spec_valid = 1;
+    }
+  }
+  GD::sync();
+  // 1. running-row summaries after the advance: one row per thread (mns <= 256 here)
+  {
+    int e = -1, rem = 0;
+    if (dt < c.n_run) {
+      const int a = c.run_rank[dt];
+      const int g = c.run_gen[dt] + (dec ? 1 : 0);
+      if (!dec || g < c.run_out[dt]) {  // a decode's finished rows leave (workload.py:134-136)
+        int lo = 0, hi = n_est;           // the list is sorted by rank
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (S.spec_rank[mid] <= a) lo = mid;
+          else hi = mid;
+        }
+        e = lo;
+        rem = S.spec_ol[e] - g;
+      }
+    }
+    const unsigned peers = __match_any_sync(kFull, e);
+    if (e >= 0) {
+      const unsigned sum = __reduce_add_sync(peers, (unsigned)rem);
+      const unsigned mx = __reduce_max_sync(peers, (unsigned)rem);
+      if (lane == __ffs(peers) - 1) {
+        atomicAdd(&S.spec_L[e], __popc(peers));
+        atomicAdd(&S.spec_rsum[e], (int)sum);
+        atomicMax(&S.spec_rmax[e], (int)mx);
+      }
+    }
+  }
+  GD::sync();
+  handoff_arrive();  // every input is read: group M may now change the running list, act, q, m
+  // 2. per-warp metadata (lane e = entry e) and the draw / PEM-segment offsets in one warp scan
+  int nunp = 0, L = 0, base = 0, ol = 0, mcb = 0, dcnt = 0, nj = 0;
+  if (lane < n_est) {
+    nunp = S.spec_nunp[lane];
+    L = S.spec_L[lane];
+    base = S.spec_base[lane];
+    ol = S.spec_ol[lane];
+    mcb = S.spec_m[lane];
+    dcnt = nunp > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
+    const unsigned tot = (unsigned)(nunp + L);
+    nj = tot > 0 ? (int)(((unsigned long long)(tot + (unsigned)pm.mns - 1u) * P.mns_magic) >> 32) : 0;
+  }
+  const int incl = warp_incl_scan((dcnt << 16) | nj);
+  const int jo = (incl & 0xFFFF) - nj, doff = (incl >> 16) - dcnt;
+  const int tot_incl = __shfl_sync(kFull, incl, 31);
+  const int D = tot_incl >> 16, J = tot_incl & 0xFFFF;
+  if (J > kMaxJobs) {  // group-uniform: every warp computed the same totals
+    if (dt == 0) S.spec_valid = 0;
+    return;
+  }
+  if (gw == 0) {
+    {
+      const unsigned nb = (unsigned)(nunp + (nunp > Ssz ? Ssz : nunp));
+      const unsigned tot_b = __reduce_add_sync(kFull, nb);
+      if (lane == 0) S.spec_alg = 4LL * tot_b;  // PEM items' + sampled tok
+    }
+    // numpy next32 positions [0, D) -> bounded draws, from the generator after this iteration's update
+    const rs_pcg64_state r0 = c.rng;
+    const unsigned h0 = r0.has_uint32;
+    const U128 s0{r0.state_hi, r0.state_lo};
+    bool rej = false;
+    {
+      const unsigned dm = __ballot_sync(kFull, lane < n_est && dcnt > 0);
+      if (lane < n_est) {
+        S.est_doff[lane] = dcnt > 0 ? doff : 0x7FFFFFFF;
+        S.est_nunp[lane] = nunp;
+        if (dcnt > 0) S.est_drawer[__popc(dm & ((1u << lane) - 1u))] = lane;
+      }
+    }
+    __syncwarp();
+    const int cnt32 = D - (int)h0 > 0 ? D - (int)h0 : 0;
+    const int n64 = (cnt32 + 1) >> 1;
+    U128 sb = s0, s_end = s0;
+    uint64_t out_end = 0;
+    for (int r0i = 0; r0i < n64; r0i += 32) {
+      const U128 st = add128(mul128(S.jstep[lane].a, sb), S.jstep[lane].c);
+      const uint64_t out = pcg_output(st);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int p = (int)h0 + 2 * (r0i + lane) + half;
+        if (p < D) {
+          const uint32_t v = half ? (uint32_t)(out >> 32) : (uint32_t)out;
+          const int kq = (int)(((unsigned)p * P.dper_magic) >> 16);  // p / dper
+          const int d = p - kq * dper;
+          const uint32_t ne = (uint32_t)S.est_nunp[S.est_drawer[kq]];
+          const uint32_t bound = d < Ssz ? ne - (uint32_t)Ssz + (uint32_t)d : (uint32_t)(Ssz - 1 - (d - Ssz));
+          const uint32_t excl = bound + 1u;
+          const uint64_t mm = (uint64_t)v * excl;
+          const uint32_t left = (uint32_t)mm;
+          if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;
+          S.small.draws[p] = (uint32_t)(mm >> 32);
+        }
+      }
+      const int last = n64 - 1 - r0i;
+      if (last < 32) {
+        s_end.hi = __shfl_sync(kFull, st.hi, last);
+        s_end.lo = __shfl_sync(kFull, st.lo, last);
+        out_end = __shfl_sync(kFull, out, last);
+      }
+      sb.hi = __shfl_sync(kFull, st.hi, 31);
+      sb.lo = __shfl_sync(kFull, st.lo, 31);
+    }
+    if (h0 && D > 0 && lane == 0) {  // position 0 is the buffered half-word
+      int e = 0;
+      for (int x = 0; x < n_est; ++x)
+        if (S.est_doff[x] <= 0) e = x;
+      const uint32_t bound = (uint32_t)S.est_nunp[e] - (uint32_t)Ssz;
+      const uint32_t excl = bound + 1u;
+      const uint64_t mm = (uint64_t)r0.uinteger * excl;
+      const uint32_t left = (uint32_t)mm;
+      if (left < excl && left < (0xFFFFFFFFu - bound) % excl) rej = true;
+      S.small.draws[0] = (uint32_t)(mm >> 32);
+    }
+    rej = __any_sync(kFull, rej);
+    __syncwarp();
+    if (rej) {  // a rejection shifts every later draw: the next iteration replays it in place
+      if (lane == 0) S.spec_valid = 0;
+    } else {
+      if (lane < n_est) {  // sample_cache_miss_ratio (prefix_cache.py:141-169), utok = tok - B*m
+        const long long mh = 16LL * mcb;
+        double ratio = 0.0;
+        if (nunp > 0) {
+          long long usum = 0, tsum = 0;
+          if (nunp <= Ssz) {
+            for (int i = 0; i < nunp; ++i) {
+              const long long t = T.tok[base + i];
+              usum += t - mh;
+              tsum += t;
+            }
+          } else {
+            tsum = floyd_tok_sum<8>(T.tok + base, S.small.draws + doff, (uint32_t)nunp);
+            usum = tsum - 8 * mh;
+          }
+          ratio = __ddiv_rn((double)usum, (double)tsum);
+        }
+        S.est_ratio[lane] = ratio;
+      }
+      if (lane == 0) {
+        rs_pcg64_state r = r0;
+        if (D > 0) {  // numpy's half-word buffer (see dpu_small)
+          if (cnt32 == 0) {
+            r.has_uint32 = 0;
+          } else {
+            r.state_hi = s_end.hi;
+            r.state_lo = s_end.lo;
+            r.has_uint32 = cnt32 & 1;
+            r.uinteger = (uint32_t)(out_end >> 32);
+          }
+        }
+        S.spec_rng = r;
+      }
+    }
+  }
+  // 3. one PEM segment per warp 1..kDWarps-1; the first segment's tok loads
+  //    are issued before the barrier, under the RNG replay
+  for (int j = gw - 1, first = 1;; j += kDWarps - 1, first = 0) {
+    const bool act = gw > 0 && j < J;
+    int e = 0, k = 0, ne = 0, Le = 0, basee = 0, ole = 0, t0 = 0, nloc = 0;
+    int uv[8];
+    if (act) {
+      const unsigned em = __ballot_sync(kFull, lane < n_est && jo <= j && nj > 0);
+      e = 31 - __clz(em);
+      k = j - __shfl_sync(kFull, jo, e);
+      ne = __shfl_sync(kFull, nunp, e);
+      Le = __shfl_sync(kFull, L, e);
+      basee = __shfl_sync(kFull, base, e);
+      ole = __shfl_sync(kFull, ol, e);
+      const int mns = (int)pm.mns;
+      t0 = k * mns - Le < 0 ? 0 : k * mns - Le;
+      nloc = ((k + 1) * mns - Le < ne ? (k + 1) * mns - Le : ne) - t0;
+    }
+    const int per = (nloc + 31) >> 5, x0 = lane * per;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) uv[i] = (act && i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
+    if (first) GD::sync();
+    if (!act) break;
+    const double ratio = S.est_ratio[e];
+    int* Uw = S.small.U[gw];
+    {
+      int ls = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uv[i] = uv[i] ? (int)utok_approx(uv[i], ratio) : 0;
+        ls += uv[i];
+      }
+      int run = warp_incl_scan(ls) - ls;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        run += uv[i];
+        if (i < per && x0 + i < nloc) Uw[x0 + i] = run;
+      }
+    }
+    __syncwarp();
+    double* tj = S.small.terms + j * kJobTerms;
+    double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
+    int nterm = 0, bb = 0, my_end = 0;
+    while (bb < nloc) {
+      const int before = bb ? Uw[bb - 1] : 0;
+      const int ub = Uw[bb];
+      const int thr = ub - before > pm.mnbt ? ub : before + (int)pm.mnbt;
+      int nb = nloc;
+      for (int b2 = bb + 1; b2 < nloc; b2 += 64) {
+        const int x = b2 + lane, y = x + 32;
+        const bool hx = x < nloc && Uw[x] > thr, hy = y < nloc && Uw[y] > thr;
+        const unsigned mx = __ballot_sync(kFull, hx), my = __ballot_sync(kFull, hy);
+        if (mx | my) {
+          nb = mx ? b2 + __ffs(mx) - 1 : b2 + 32 + __ffs(my) - 1;
+          break;
+        }
+      }
+      if (nterm < 32) {
+        if (lane == nterm) my_end = nb;
+      } else if (lane == 0) {
+        const double t = lin(pm.ap, (double)(Uw[nb - 1] - before), pm.bp);
+        if (nterm < kJobTerms) tj[nterm] = t;
+        else spill[nterm] = t;
+      }
+      ++nterm;
+      bb = nb;
+    }
+    {
+      const int beg = __shfl_up_sync(kFull, my_end, 1);
+      if (lane < nterm && lane < 32) {
+        const int b0 = lane ? beg : 0;
+        tj[lane] = lin(pm.ap, (double)(Uw[my_end - 1] - (b0 ? Uw[b0 - 1] : 0)), pm.bp);
+      }
+    }
+    if (lane == 0) {
+      long long rs = (long long)nloc * ole;
+      long long mx = nloc > 0 ? ole : 0;
+      if (k == 0) {  // the running rows enter the first segment as a prefilled summary
+        rs += S.spec_rsum[e];
+        mx = S.spec_rmax[e] > mx ? S.spec_rmax[e] : mx;
+      }
+      const double t = __dadd_rn(__dmul_rn(pm.ad, (double)rs), __dmul_rn(pm.bd, (double)mx));
+      if (nterm < kJobTerms) tj[nterm] = t;
+      else spill[nterm] = t;
+      S.small.nterm[j] = nterm + 1;
+    }
+    __syncwarp();
+  }
+  GD::sync();
+  if (gw == 0 && lane < n_est) {  // ordered sums, entry by entry
+    double total = 0.0;
+    for (int j = jo; j < jo + nj; ++j) {
+      const int cnt = S.small.nterm[j];
+      const double* tj = S.small.terms + j * kJobTerms;
+      const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
+      const int nsm = cnt < kJobTerms ? cnt : kJobTerms;
+#pragma unroll 4
+      for (int i = 0; i < nsm; ++i) total = __dadd_rn(total, tj[i]);
+#pragma unroll 1
+      for (int i = nsm; i < cnt; ++i) total = __dadd_rn(total, spill[i]);
+    }
+    S.spec_val[lane] = total;
+  }
+}
+
+// After the join (warp 0): the speculative update becomes this (next)
+// iteration's if every chain length it assumed is the advance's; retiring
+// relQueries (no unprefilled and no running row left) are not written.  The
+// entries kept must be exactly the advance's act list.
+__device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const int lane = threadIdx.x & 31;
+  bool ok = S.spec_valid && c.status == RS_RUNNING;
+  const int n = S.spec_n;
+  bool keep = false, bad = false;
+  int a = 0;
+  if (ok && lane < n) {
+    a = S.spec_rank[lane];
+    keep = S.spec_nunp[lane] > 0 || S.spec_L[lane] > 0;
+    bad = keep && ((S.spec_nunp[lane] > 0 && rq.m[a] != S.spec_m[lane]) ||
+                   c.act[__popc(__ballot_sync(__activemask(), keep) & ((1u << lane) - 1u))] != a);
+  }
+  const unsigned km = __ballot_sync(kFull, keep);
+  ok = ok && !__any_sync(kFull, bad) && __popc(km) == c.n_act;
+  if (ok && keep) rq.prio[a] = S.spec_val[lane];
+  if (lane == 0) {
+    if (ok) {
+      c.rng = S.spec_rng;
+      c.alg_bytes += S.spec_alg;
+    }
+    S.spec_ok = ok;
+  }
+}
+
 // First sight of this iteration's arrivals [new_lo, new_hi): none of their
 // rows is prefilled and their shared chain is not resident (no row of theirs
 // was ever inserted), so the sampled uncached-token ratio is exactly 1.0 and

@@ -171,12 +171,215 @@ __device__ __forceinline__ double world_duration(const Params& P, const TraceDev
   return base;
 }
 
+// ---- F: execute the decided action (engine.py:315-363, 435-448) on warp
+// group G (the whole CTA, or group M of the pipelined common-configuration
+// iteration, which waits at the handoff barrier (kHand) before its first write
+// of state group D reads).  Returns false when the trace stopped.
+template <bool kC, class G, bool kHand>
+__device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shared& S, const int action) {
+  Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const int tid = threadIdx.x;
+  const rs_config& cfg = P.cfg;
+  if (action == RS_ACTION_PREFILL) {  // _execute_prefill (engine.py:315-341)
+    const int h = S.head;
+    const int q = rq.q[h];
+    const int row0 = rq.off[h] + q;
+    const int n = S.taken;
+    const int n_run0 = c.n_run;
+    const int ol = rq.ol[h];
+    long long ut = 0;
+    const bool fast = prefill_fast<kC, G, kHand>(P, T, S, h, n, S.cand_tok, ut);
+    if (kHand && !fast) handoff_wait();  // the exact per-row path changes rq.m too
+    phase_mark(c, 9);
+    if (tid == 0) {
+      bool ok = c.status == RS_RUNNING;
+      if (!fast && ok) {
+        for (int i = 0; i < n; ++i) {
+          const long long u = prefill_row_cache(c, T, rq, P, h, S.cand_tok[i]);
+          if (u < 0) {
+            ok = false;
+            break;
+          }
+          ut += u;
+        }
+      }
+      if (ok) {
+        c.alg_bytes += 16LL * n;  // FIFO pushes (window reads are counted in prefill_fast)
+        const double start = c.clock;
+        const double dur =
+            world_duration<kC>(P, T, c.n_batch++, __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p));
+        c.n_run = n_run0 + n;
+        rq.q[h] = q + n;
+        if (h == c.zh_idx) c.zh_valid = 0;  // the cached static-order head may have left the order
+        if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
+        if (rq.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
+        rq.nrun[h] += n;
+        if (q == 0 && (kC || P.use_dpu)) {  // becomes partially prefilled: join the re-estimate list
+          int pos = c.n_act;
+          if (pos >= kMaxAct) {
+            c.status = RS_EUNSUPPORTED;
+            c.error_detail = 3;
+          } else {
+            while (pos > 0 && c.act[pos - 1] > h) {
+              c.act[pos] = c.act[pos - 1];
+              --pos;
+            }
+            c.act[pos] = h;
+            c.n_act++;
+          }
+        }
+        c.clock = __dadd_rn(c.clock, dur);
+        if (q == 0) T.fps[h] = start;  // first_prefill_start is set once (engine.py:338-339)
+        T.lpe[h] = c.clock;
+        if (kC || (cfg.log_decisions && T.log_cap > 0)) {
+          rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
+          r.batch_rq = h;
+          r.batch_first = q;
+          r.batch_n = n;
+        }
+      }
+      S.go = ok && c.status == RS_RUNNING;
+    }
+    // running list append + kv reservation (engine.py:326-329): sum of
+    // (tok + output_limit) = candidate kv prefix at n-1
+    for (int i = tid; i < n; i += G::kN) {
+      c.run_row[n_run0 + i] = row0 + i;
+      c.run_rank[n_run0 + i] = h;
+      c.run_gen[n_run0 + i] = 0;
+      c.run_out[n_run0 + i] = S.cand_out[i];
+      c.run_kv[n_run0 + i] = S.cand_tok[i] + ol;
+    }
+    if (tid == 0) c.kv += (long long)S.cand_u[n - 1] + (long long)n * (S.cand_mh + ol);
+    G::sync();
+    phase_mark(c, 10);
+    if (!S.go) return false;
+  } else if (action == RS_ACTION_DECODE) {  // _execute_decode (engine.py:343-363)
+    const int n = c.n_run;
+    if (tid == 0) {
+      S.act_dirty = 0;
+      S.rrq_dirty = 0;
+    }
+    G::sync();
+    const double clk = __dadd_rn(
+        c.clock, world_duration<kC>(P, T, c.n_batch, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d)));
+    int kv_free = 0;
+    int keep[kMaxRun / G::kN], nrow[kMaxRun / G::kN], nrank[kMaxRun / G::kN];
+    int ngen[kMaxRun / G::kN], nout[kMaxRun / G::kN], nkv[kMaxRun / G::kN];
+#pragma unroll
+    for (int s = 0; s < kMaxRun / G::kN; ++s) {
+      const int j = s * G::kN + tid;
+      keep[s] = 0;
+      if (j < n) {
+        const int r = c.run_row[j];
+        const int a = c.run_rank[j];
+        const int g = c.run_gen[j] + 1;
+        nrow[s] = r;
+        nrank[s] = a;
+        ngen[s] = g;
+        nout[s] = c.run_out[j];
+        nkv[s] = c.run_kv[j];
+        if (g >= nout[s]) {  // done (workload.py:134-136)
+          T.gen[r] = g;
+          T.comp[r] = (int)c.iteration;
+          kv_free += nkv[s];
+          if (atomicSub(&rq.nrun[a], 1) == 1) S.rrq_dirty = 1;
+          if (atomicAdd(&rq.ndone[a], 1) + 1 == rq.off[a + 1] - rq.off[a]) {
+            T.lde[a] = clk;  // relQuery retired (engine.py:360-362)
+            atomicSub(&c.live, 1);
+            S.act_dirty = 1;
+          }
+        } else {
+          keep[s] = 1;
+        }
+      }
+    }
+    // stable compaction of the running list + freed kv, one fused scan per
+    // tile (the scan's first barrier orders all reads of the old list)
+    if constexpr (kHand) handoff_wait();  // group D has read the running list and the act list
+    int cbase = 0;
+    long long kv_total = 0;
+#pragma unroll
+    for (int s = 0; s < kMaxRun / G::kN; ++s) {
+      if (s * G::kN < n) {
+        int v[2] = {keep[s], (int)kv_free}, tot[2];
+        kv_free = 0;
+        group_scan32<G, 2>(v, S.s32, tot, tid >> 5);
+        if (keep[s]) {
+          const int d = cbase + v[0] - 1;
+          c.run_row[d] = nrow[s];
+          c.run_rank[d] = nrank[s];
+          c.run_gen[d] = ngen[s];
+          c.run_out[d] = nout[s];
+          c.run_kv[d] = nkv[s];
+        }
+        cbase += tot[0];
+        kv_total += tot[1];
+      }
+    }
+    G::sync();
+    if (tid == 0) {
+      c.alg_bytes += 8LL * (n - cbase);  // generated + completion iteration of finished rows
+      c.n_run = cbase;
+      c.kv -= kv_total;
+      c.clock = clk;
+      c.n_batch++;
+      if (kC || (cfg.log_decisions && T.log_cap > 0)) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
+      if (S.rrq_dirty) {
+        int w = 0;
+        for (int i = 0; i < c.n_rrq; ++i)
+          if (rq.nrun[c.rrq[i]] > 0) c.rrq[w++] = c.rrq[i];
+        c.n_rrq = w;
+      }
+      if (S.act_dirty && (kC || P.use_dpu)) {  // drop retired relQueries from the re-estimate list
+        int w = 0;
+        for (int i = 0; i < c.n_act; ++i) {
+          const int a = c.act[i];
+          if (rq.ndone[a] < rq.off[a + 1] - rq.off[a]) c.act[w++] = a;
+        }
+        c.n_act = w;
+      }
+    }
+  } else {  // idle (engine.py:439-447)
+    if constexpr (kHand) handoff_wait();
+    if (tid == 0) {
+      if (c.n_admitted >= T.R) {
+        c.status = c.live ? RS_EABORT_IDLE : RS_OK;
+        S.go = 0;
+        if (kC || (cfg.log_decisions && T.log_cap > 0)) {
+          T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
+          c.n_log++;
+        }
+      } else {
+        const double nxt = rq.arrival[c.n_admitted];
+        if (nxt > c.clock) c.clock = nxt;
+        S.go = 1;
+      }
+    }
+    G::sync();
+    if (!S.go) return false;
+  }
+  if (tid == 0) {
+    if (kC || (cfg.log_decisions && T.log_cap > 0)) {
+      T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
+      c.n_log++;
+    }
+    c.iteration++;
+    S.pf_head = S.head;  // read after the next admission barrier
+  }
+  phase_mark(c, 4);
+  // no closing barrier: the next admission (thread 0) touches nothing the other threads
+  // still read here (its flag is S.go_admit, not the execution phase's S.go)
+  return true;
+  return true;
+}
+
 // kC: the common configuration, fixed at compile time (a DPU policy, tau = inf,
 // no world-model noise, one shard, decision log on,
 // the default block size 16 and sample size 8):
 // the checks for everything else leave the iteration's instruction stream.
 template <bool kFast, bool kC>
-__device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
+__device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const bool last) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const int tid = threadIdx.x;
@@ -238,7 +441,14 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
 
   // ---- B: priorities.  fcfs: 0.0; sp: static_relquery_prio, both set at
   // admission (engine.py:255-267, preloaded into prio); relserve*: the DPU.
-  if (kC || P.use_dpu) {
+  if constexpr (kC) {
+    if (!S.spec_ok) {  // the launch's first iteration, or the speculative update was not usable
+      dpu_update<kFast, kC>(P, T, S);
+    } else {  // the re-estimates were computed during the previous advance: only the arrivals remain
+      if (S.new_hi > S.new_lo) first_sight(P, T, S, S.new_lo, S.new_hi);
+      if (tid == 0) S.n_est = c.n_act + (S.new_hi - S.new_lo);
+    }
+  } else if (P.use_dpu) {
     dpu_update<kFast, kC>(P, T, S);
   } else if (tid == 0) {
     S.n_est = 0;
@@ -510,193 +720,23 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S) {
   phase_mark(c, 3);
 
   // ---- F: execute
-  if (action == RS_ACTION_PREFILL) {  // _execute_prefill (engine.py:315-341)
-    const int h = S.head;
-    const int q = rq.q[h];
-    const int row0 = rq.off[h] + q;
-    const int n = S.taken;
-    const int n_run0 = c.n_run;
-    const int ol = rq.ol[h];
-    long long ut = 0;
-    const bool fast = prefill_fast<kC>(P, T, S, h, n, S.cand_tok, ut);
-    phase_mark(c, 9);
-    if (tid == 0) {
-      bool ok = c.status == RS_RUNNING;
-      if (!fast && ok) {
-        for (int i = 0; i < n; ++i) {
-          const long long u = prefill_row_cache(c, T, rq, P, h, S.cand_tok[i]);
-          if (u < 0) {
-            ok = false;
-            break;
-          }
-          ut += u;
-        }
-      }
-      if (ok) {
-        c.alg_bytes += 16LL * n;  // FIFO pushes (window reads are counted in prefill_fast)
-        const double start = c.clock;
-        const double dur =
-            world_duration<kC>(P, T, c.n_batch++, __dadd_rn(__dmul_rn(P.world.alpha_p, (double)ut), P.world.beta_p));
-        c.n_run = n_run0 + n;
-        rq.q[h] = q + n;
-        if (h == c.zh_idx) c.zh_valid = 0;  // the cached static-order head may have left the order
-        if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
-        if (rq.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
-        rq.nrun[h] += n;
-        if (q == 0 && (kC || P.use_dpu)) {  // becomes partially prefilled: join the re-estimate list
-          int pos = c.n_act;
-          if (pos >= kMaxAct) {
-            c.status = RS_EUNSUPPORTED;
-            c.error_detail = 3;
-          } else {
-            while (pos > 0 && c.act[pos - 1] > h) {
-              c.act[pos] = c.act[pos - 1];
-              --pos;
-            }
-            c.act[pos] = h;
-            c.n_act++;
-          }
-        }
-        c.clock = __dadd_rn(c.clock, dur);
-        if (q == 0) T.fps[h] = start;  // first_prefill_start is set once (engine.py:338-339)
-        T.lpe[h] = c.clock;
-        if (kC || (cfg.log_decisions && T.log_cap > 0)) {
-          rs_iter_record& r = T.log[c.n_log & (T.log_cap - 1)];
-          r.batch_rq = h;
-          r.batch_first = q;
-          r.batch_n = n;
-        }
-      }
-      S.go = ok && c.status == RS_RUNNING;
-    }
-    // running list append + kv reservation (engine.py:326-329): sum of
-    // (tok + output_limit) = candidate kv prefix at n-1
-    for (int i = tid; i < n; i += kThreads) {
-      c.run_row[n_run0 + i] = row0 + i;
-      c.run_rank[n_run0 + i] = h;
-      c.run_gen[n_run0 + i] = 0;
-      c.run_out[n_run0 + i] = S.cand_out[i];
-      c.run_kv[n_run0 + i] = S.cand_tok[i] + ol;
-    }
-    if (tid == 0) c.kv += (long long)S.cand_u[n - 1] + (long long)n * (S.cand_mh + ol);
-    __syncthreads();
-    phase_mark(c, 10);
-    if (!S.go) return false;
-  } else if (action == RS_ACTION_DECODE) {  // _execute_decode (engine.py:343-363)
-    const int n = c.n_run;
-    if (tid == 0) {
-      S.act_dirty = 0;
-      S.rrq_dirty = 0;
+  if constexpr (kC) {
+    // pipelined: group M executes this iteration while group D computes the
+    // next iteration's priority update of the partially prefilled relQueries
+    // (dpu_spec) from the state this advance leaves; both join at the barrier
+    const bool allowed = !last && c.iteration + 1 < cfg.iteration_limit;
+    if (opaque_warp() < kMWarps) {
+      const bool go = execute<kC, GM, true>(P, T, S, action);  // group-uniform
+      if (tid == 0) S.go_exec = go;
+    } else {
+      dpu_spec(P, T, S, action, S.head, S.taken, allowed);
     }
     __syncthreads();
-    const double clk = __dadd_rn(
-        c.clock, world_duration<kC>(P, T, c.n_batch, __dadd_rn(__dmul_rn(P.world.alpha_d, (double)n), P.world.beta_d)));
-    int kv_free = 0;
-    int keep[kMaxRun / kThreads], nrow[kMaxRun / kThreads], nrank[kMaxRun / kThreads];
-    int ngen[kMaxRun / kThreads], nout[kMaxRun / kThreads], nkv[kMaxRun / kThreads];
-#pragma unroll
-    for (int s = 0; s < kMaxRun / kThreads; ++s) {
-      const int j = s * kThreads + tid;
-      keep[s] = 0;
-      if (j < n) {
-        const int r = c.run_row[j];
-        const int a = c.run_rank[j];
-        const int g = c.run_gen[j] + 1;
-        nrow[s] = r;
-        nrank[s] = a;
-        ngen[s] = g;
-        nout[s] = c.run_out[j];
-        nkv[s] = c.run_kv[j];
-        if (g >= nout[s]) {  // done (workload.py:134-136)
-          T.gen[r] = g;
-          T.comp[r] = (int)c.iteration;
-          kv_free += nkv[s];
-          if (atomicSub(&rq.nrun[a], 1) == 1) S.rrq_dirty = 1;
-          if (atomicAdd(&rq.ndone[a], 1) + 1 == rq.off[a + 1] - rq.off[a]) {
-            T.lde[a] = clk;  // relQuery retired (engine.py:360-362)
-            atomicSub(&c.live, 1);
-            S.act_dirty = 1;
-          }
-        } else {
-          keep[s] = 1;
-        }
-      }
-    }
-    // stable compaction of the running list + freed kv, one fused scan per
-    // tile (the scan's first barrier orders all reads of the old list)
-    int cbase = 0;
-    long long kv_total = 0;
-#pragma unroll
-    for (int s = 0; s < kMaxRun / kThreads; ++s) {
-      if (s * kThreads < n) {
-        int v[2] = {keep[s], (int)kv_free}, tot[2];
-        kv_free = 0;
-        block_scan32<2>(v, S.s32, tot);
-        if (keep[s]) {
-          const int d = cbase + v[0] - 1;
-          c.run_row[d] = nrow[s];
-          c.run_rank[d] = nrank[s];
-          c.run_gen[d] = ngen[s];
-          c.run_out[d] = nout[s];
-          c.run_kv[d] = nkv[s];
-        }
-        cbase += tot[0];
-        kv_total += tot[1];
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      c.alg_bytes += 8LL * (n - cbase);  // generated + completion iteration of finished rows
-      c.n_run = cbase;
-      c.kv -= kv_total;
-      c.clock = clk;
-      c.n_batch++;
-      if (kC || (cfg.log_decisions && T.log_cap > 0)) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
-      if (S.rrq_dirty) {
-        int w = 0;
-        for (int i = 0; i < c.n_rrq; ++i)
-          if (rq.nrun[c.rrq[i]] > 0) c.rrq[w++] = c.rrq[i];
-        c.n_rrq = w;
-      }
-      if (S.act_dirty && (kC || P.use_dpu)) {  // drop retired relQueries from the re-estimate list
-        int w = 0;
-        for (int i = 0; i < c.n_act; ++i) {
-          const int a = c.act[i];
-          if (rq.ndone[a] < rq.off[a + 1] - rq.off[a]) c.act[w++] = a;
-        }
-        c.n_act = w;
-      }
-    }
-  } else {  // idle (engine.py:439-447)
-    if (tid == 0) {
-      if (c.n_admitted >= T.R) {
-        c.status = c.live ? RS_EABORT_IDLE : RS_OK;
-        S.go = 0;
-        if (kC || (cfg.log_decisions && T.log_cap > 0)) {
-          T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
-          c.n_log++;
-        }
-      } else {
-        const double nxt = rq.arrival[c.n_admitted];
-        if (nxt > c.clock) c.clock = nxt;
-        S.go = 1;
-      }
-    }
-    __syncthreads();
-    if (!S.go) return false;
+    if (opaque_warp() == 0) spec_commit(S, T);
+    return S.go_exec;
+  } else {
+    return execute<kC, GAll, false>(P, T, S, action);
   }
-  if (tid == 0) {
-    if (kC || (cfg.log_decisions && T.log_cap > 0)) {
-      T.log[c.n_log & (T.log_cap - 1)].kv_reserved = c.kv;
-      c.n_log++;
-    }
-    c.iteration++;
-    S.pf_head = S.head;  // read after the next admission barrier
-  }
-  phase_mark(c, 4);
-  // no closing barrier: the next admission (thread 0) touches nothing the other threads
-  // still read here (its flag is S.go_admit, not the execution phase's S.go)
-  return true;
 }
 
 __device__ __forceinline__ void copy16(void* dst, const void* src, size_t bytes) {
@@ -722,12 +762,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   if (threadIdx.x == 0) {
     S.rq = rq_carve(rq_base, T.R);
     S.pf_head = -1;  // no previous head to prefetch for
+    S.spec_ok = 0;   // the launch's first update runs in place (dpu_update)
   }
   __syncthreads();
   if (S.c.status == RS_RUNNING) {
     if (threadIdx.x == 0) S.c.phase[kPhases - 1] = clock64();
     for (long long it = 0; it < P.max_iters; ++it)
-      if (!iterate<kFast, kC>(P, T, S)) break;
+      if (!iterate<kFast, kC>(P, T, S, it + 1 == P.max_iters)) break;
   }
   __syncthreads();
   // running rows' generated counts back to HBM (finished rows were written at completion)

@@ -197,6 +197,7 @@ struct Shared {
   JumpEntry jt[kJumpBits];
   JumpEntry jstep[32];  // (A^k, C_k) for k = 1..32 steps
   int go, action;
+  int go_exec;  // the pipelined iteration's execution result (group M -> everyone after the join)
   int go_admit;  // phase A's continue flag (separate from `go`: no barrier closes an iteration)
   int new_lo, new_hi;
   int head, W, taken, J;
@@ -222,6 +223,23 @@ struct Shared {
   int rng_reject;
   unsigned long long rej_pos;  // first-sight replay: first stream position with a Lemire rejection
   int new_lo_rs;               // ... and the arrival its parallel replay restarts at
+  // pipelined priority update (common configuration): group D computes the next
+  // iteration's update of the partially prefilled relQueries during this
+  // iteration's state advance (dpu.cuh dpu_spec); committed after the join
+  int spec_ok;    // this iteration's update of c.act is already done (committed)
+  int spec_valid; // group D's verdict on its result (fits the fast path, no Lemire rejection)
+  int spec_n;     // entries of the speculative list
+  int spec_rank[kSmallEst];
+  int spec_m[kSmallEst];     // chain length its ratio assumed (checked against the advance's)
+  int spec_nunp[kSmallEst];  // unprefilled rows after the advance
+  int spec_base[kSmallEst];  // first unprefilled row
+  int spec_ol[kSmallEst];
+  int spec_L[kSmallEst];     // running rows after the advance: count, sum and max of remaining
+  int spec_rsum[kSmallEst];
+  int spec_rmax[kSmallEst];
+  double spec_val[kSmallEst];
+  rs_pcg64_state spec_rng;
+  long long spec_alg;
   // batched prefill eviction
   int fp_bad, fp_popped, fp_par, fp_cut;
   long long fp_rem;
@@ -235,20 +253,22 @@ struct Shared {
       int REM[kItemBuf];
       int jcnt[kItemBuf + kEstBatch];
     } seg;
-    struct {
-      unsigned int draws[kSmallEst * 31];
-      double terms[kMaxJobs * kJobTerms];
-      int nterm[kMaxJobs];
-      int U[kWarps][kSmallMns];  // per-warp utok prefix of the segment it evaluates
-    } small;
-    struct {
-      unsigned long long t0[kWin];
-      unsigned long long c0[kWin];
-      int rank[kWin];
-      int tres[kWin];
-      int mm[kWin];
-      int last[kWin];  // 1 if this is the rank's last resident tail
-    } win;
+    struct {  // side by side: the pipelined iteration runs the DPU fast path and the prefill advance at once
+      struct {
+        unsigned int draws[kSmallEst * 31];
+        double terms[kMaxJobs * kJobTerms];
+        int nterm[kMaxJobs];
+        int U[kWarps][kSmallMns];  // per-warp utok prefix of the segment it evaluates
+      } small;
+      struct {
+        unsigned long long t0[kWin];
+        unsigned long long c0[kWin];
+        int rank[kWin];
+        int tres[kWin];
+        int mm[kWin];
+        int last[kWin];  // 1 if this is the rank's last resident tail
+      } win;
+    };
   };
   // relQuery table follows (dynamic shared memory) when rq_in_smem
 };
