@@ -490,11 +490,12 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
 // dpu_update in place.
 __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const int action, const int h, const int nh,
                          const bool allowed) {
-  const Ctl& c = S.c;
+  Ctl& c = S.c;
   const RqView rq = S.rq;
   const int lane = threadIdx.x & 31, gw = opaque_warp() - kMWarps;
   const int dt = threadIdx.x - kMWarps * 32;
   const bool pf = action == RS_ACTION_PREFILL, dec = action == RS_ACTION_DECODE;
+  dphase_mark(c, -1);
   const int n_act = c.n_act;
   const bool join = pf && rq.q[h] == 0;  // h's first prefill: it joins the list
   const int n_est = n_act + (join ? 1 : 0);
@@ -543,6 +544,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
   }
   GD::sync();
+  dphase_mark(c, 5);
   // 1. running-row summaries after the advance: one row per thread (mns <= 256 here)
   {
     int e = -1, rem = 0;
@@ -572,7 +574,9 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
   }
   GD::sync();
+  dphase_mark(c, 6);
   handoff_arrive();  // every input is read: group M may now change the running list, act, q, m
+  dphase_mark(c, 19);
   // 2. per-warp metadata (lane e = entry e) and the draw / PEM-segment offsets in one warp scan
   int nunp = 0, L = 0, base = 0, ol = 0, mcb = 0, dcnt = 0, nj = 0;
   if (lane < n_est) {
@@ -589,6 +593,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   const int jo = (incl & 0xFFFF) - nj, doff = (incl >> 16) - dcnt;
   const int tot_incl = __shfl_sync(kFull, incl, 31);
   const int D = tot_incl >> 16, J = tot_incl & 0xFFFF;
+  dphase_mark(c, 7);
   if (J > kMaxJobs) {  // group-uniform: every warp computed the same totals
     if (dt == 0) S.spec_valid = 0;
     return;
@@ -616,6 +621,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     const int cnt32 = D - (int)h0 > 0 ? D - (int)h0 : 0;
     const int n64 = (cnt32 + 1) >> 1;
     U128 sb = s0, s_end = s0;
+    dphase_mark(c, 8);
     uint64_t out_end = 0;
     for (int r0i = 0; r0i < n64; r0i += 32) {
       const U128 st = add128(mul128(S.jstep[lane].a, sb), S.jstep[lane].c);
@@ -658,6 +664,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
     rej = __any_sync(kFull, rej);
     __syncwarp();
+    dphase_mark(c, 9);
     if (rej) {  // a rejection shifts every later draw: the next iteration replays it in place
       if (lane == 0) S.spec_valid = 0;
     } else {
@@ -680,6 +687,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
         }
         S.est_ratio[lane] = ratio;
       }
+      dphase_mark(c, 11);
       if (lane == 0) {
         rs_pcg64_state r = r0;
         if (D > 0) {  // numpy's half-word buffer (see dpu_small)
@@ -717,7 +725,11 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     const int per = (nloc + 31) >> 5, x0 = lane * per;
 #pragma unroll
     for (int i = 0; i < 8; ++i) uv[i] = (act && i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
-    if (first) GD::sync();
+    if (first) {
+      GD::sync();
+      dphase_mark(c, 20);
+      dphase_mark(c, 12);
+    }
     if (!act) break;
     const double ratio = S.est_ratio[e];
     int* Uw = S.small.U[gw];
@@ -786,6 +798,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   }
   GD::sync();
   if (gw == 0 && lane < n_est) {  // ordered sums, entry by entry
+  dphase_mark(c, 13);
     double total = 0.0;
     for (int j = jo; j < jo + nj; ++j) {
       const int cnt = S.small.nterm[j];
@@ -799,6 +812,8 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
     S.spec_val[lane] = total;
   }
+  dphase_mark(c, 14);
+  dphase_mark(c, 21);
 }
 
 // After the join (warp 0): the speculative update becomes this (next)

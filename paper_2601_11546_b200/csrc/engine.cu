@@ -732,6 +732,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       dpu_spec(P, T, S, action, S.head, S.taken, allowed);
     }
     __syncthreads();
+    phase_mark(c, 1);  // the wait for group D beyond the advance (the update's share of the critical path)
     if (opaque_warp() == 0) spec_commit(S, T);
     return S.go_exec;
   } else {
@@ -750,6 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ TraceDev Tsm;  // the trace's pointers, read on every access
   Shared& S = *reinterpret_cast<Shared*>(smem_raw);
+
   if (threadIdx.x == 0) Tsm = P.traces[blockIdx.x];
   __syncthreads();
   const TraceDev& T = Tsm;

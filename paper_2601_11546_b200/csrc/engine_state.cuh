@@ -324,4 +324,25 @@ __device__ __forceinline__ void phase_mark(Ctl& c, int k) {
 #endif
 }
 
+// Group D's own marks (slots 19-21, scratch stamp in slot 22) when built with
+// -DRS_DPHASE=1: the pipelined priority update's list + summaries, metadata +
+// RNG + ratios, PEM + ordered sums.
+#ifndef RS_DPHASE
+#define RS_DPHASE 0
+#endif
+// -DRS_DPHASE=2 (with RS_PHASE_TIMERS=1): also fine marks in slots 5-14.
+__device__ __forceinline__ void dphase_mark(Ctl& c, int k) {
+#if RS_DPHASE
+  if (RS_DPHASE < 2 && k >= 5 && k < 19) return;
+  if (threadIdx.x == kMWarps * 32) {
+    const long long now = clock64();
+    if (k >= 0) c.phase[k] += now - c.phase[22];
+    c.phase[22] = now;
+  }
+#else
+  (void)c;
+  (void)k;
+#endif
+}
+
 }  // namespace rsd
