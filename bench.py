@@ -434,12 +434,10 @@ def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, s
             from paper_2601_11546_b200 import sharded
 
             sharded.connect(eng)
-        eng.chunk_iterations = I
         t1 = time.perf_counter()
         eng.step(WINDOW_START)
         t15 = time.perf_counter()
-        while eng.iteration < it_end:  # up to the device window's last iteration, I per step
-            eng.step(min(I, it_end - eng.iteration))
+        eng.step(it_end - eng.iteration)  # up to the device window's last iteration (the API launches in chunks)
         t2 = time.perf_counter()
         eng._collect(0.0)
         torch.cuda.synchronize(dev)
@@ -456,11 +454,12 @@ def e2e_runs(args, trace, world, cfg, m, dev, local, stream, ws, pool, shards, s
                                       "collect_ms": 1e3 * (t3 - t2)}})
     med = sorted(runs, key=lambda r: r["value"])[len(runs) // 2]
     h2d = sum(v.nbytes for v in m.arrays.values() if v is not None)
-    n_steps = -(-(it_end - WINDOW_START) // I) + 1  # launches of the run (the first: iterations [0, 5))
-    d2h_step = I * 96 + 128
-    d2h_final = c.num_requests * 4 + c.num_relqueries * 32
+    # bytes per bench step (I iterations) of the run: the trace upload and the final readback
+    # spread over the run's iterations, plus each iteration's 96-byte decision record
+    n_launch = -(-(it_end - WINDOW_START) // Engine.chunk_iterations) + 1
+    d2h_total = it_end * 96 + n_launch * 128 + c.num_requests * 4 + c.num_relqueries * 32
     return {"value": med["value"], "unit": "iters/s",
-            "h2d_bytes_per_step": int(h2d / n_steps), "d2h_bytes_per_step": int(d2h_step + d2h_final / n_steps),
+            "h2d_bytes_per_step": int(h2d * I / it_end), "d2h_bytes_per_step": int(d2h_total * I / it_end),
             "window": [0, it_end],
             "iterations": med["iterations"], "wall_s": med["wall_s"], "breakdown_ms": med["breakdown_ms"],
             "runs": [{"value": round(r["value"], 1), **{k: round(v, 2) for k, v in r["breakdown_ms"].items()}}

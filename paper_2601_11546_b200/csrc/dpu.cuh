@@ -493,14 +493,13 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   Ctl& c = S.c;
   const RqView rq = S.rq;
   const int lane = threadIdx.x & 31, gw = opaque_warp() - kMWarps;
-  const int dt = threadIdx.x - kMWarps * 32;
   const bool pf = action == RS_ACTION_PREFILL, dec = action == RS_ACTION_DECODE;
   dphase_mark(c, -1);
   const int n_act = c.n_act;
   const bool join = pf && rq.q[h] == 0;  // h's first prefill: it joins the list
   const int n_est = n_act + (join ? 1 : 0);
   if (!allowed || n_est > kSmallEst || n_est == 0) {  // group-uniform
-    if (dt == 0) {
+    if (threadIdx.x == kMWarps * 32) {
       S.spec_valid = n_est == 0 && allowed;  // nothing to re-estimate: trivially done
       S.spec_n = 0;
       S.spec_rng = c.rng;
@@ -518,25 +517,43 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   pm.cap = P.cfg.cap;
   pm.mns = P.cfg.max_num_seqs;
   pm.mnbt = P.cfg.max_num_batched_tokens;
-  // 0. the list and each entry's state after the advance
+  // 0. the list (act, with h inserted in rank order on its first prefill) and
+  //    each entry's state after the advance; the draw offsets (they depend on
+  //    the unprefilled counts only)
   if (gw == 0) {
     const int x = lane < n_act ? c.act[lane] : 0x7FFFFFFF;
     const int pos = join ? __popc(__ballot_sync(kFull, x < h)) : 32;
     const int xm1 = __shfl_up_sync(kFull, x, 1);
     const int a = lane < pos ? x : (lane == pos ? h : xm1);
+    int nunp = 0;
     if (lane < n_est) {
       const int off = rq.off[a], size = rq.off[a + 1] - off;
       const bool isH = pf && a == h;
       const int q = rq.q[a] + (isH ? nh : 0);
       const int ol = rq.ol[a];
+      nunp = size - q;
       S.spec_rank[lane] = a;
       S.spec_m[lane] = isH ? rq.chain[a] : rq.m[a];
-      S.spec_nunp[lane] = size - q;
+      S.spec_nunp[lane] = nunp;
       S.spec_base[lane] = off + q;
       S.spec_ol[lane] = ol;
       S.spec_L[lane] = isH ? nh : 0;  // the batch's rows join the running set, remaining = output_limit
       S.spec_rsum[lane] = isH ? nh * ol : 0;
       S.spec_rmax[lane] = isH ? ol : 0;
+    }
+    const int dcnt = lane < n_est && nunp > Ssz ? dper : 0;  // choice() only when k = S < n
+    const int dincl = warp_incl_scan(dcnt);
+    const unsigned dm = __ballot_sync(kFull, dcnt > 0);
+    if (lane < n_est) {
+      S.est_doff[lane] = dcnt > 0 ? dincl - dcnt : 0x7FFFFFFF;
+      S.est_nunp[lane] = nunp;
+      if (dcnt > 0) S.est_drawer[__popc(dm & ((1u << lane) - 1u))] = lane;
+    }
+    if (lane == 31) S.spec_draws = dincl;
+    {  // the PEM items' and the sampled rows' tok
+      const unsigned nb = (unsigned)(nunp + (nunp > Ssz ? Ssz : nunp));
+      const unsigned tot_b = __reduce_add_sync(kFull, nb);
+      if (lane == 0) S.spec_alg = 4LL * tot_b;
     }
     if (lane == 0) {
       S.spec_n = n_est;
@@ -545,83 +562,18 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   }
   GD::sync();
   dphase_mark(c, 5);
-  // 1. running-row summaries after the advance: one row per thread (mns <= 256 here)
-  {
-    int e = -1, rem = 0;
-    if (dt < c.n_run) {
-      const int a = c.run_rank[dt];
-      const int g = c.run_gen[dt] + (dec ? 1 : 0);
-      if (!dec || g < c.run_out[dt]) {  // a decode's finished rows leave (workload.py:134-136)
-        int lo = 0, hi = n_est;           // the list is sorted by rank
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (S.spec_rank[mid] <= a) lo = mid;
-          else hi = mid;
-        }
-        e = lo;
-        rem = S.spec_ol[e] - g;
-      }
-    }
-    const unsigned peers = __match_any_sync(kFull, e);
-    if (e >= 0) {
-      const unsigned sum = __reduce_add_sync(peers, (unsigned)rem);
-      const unsigned mx = __reduce_max_sync(peers, (unsigned)rem);
-      if (lane == __ffs(peers) - 1) {
-        atomicAdd(&S.spec_L[e], __popc(peers));
-        atomicAdd(&S.spec_rsum[e], (int)sum);
-        atomicMax(&S.spec_rmax[e], (int)mx);
-      }
-    }
-  }
-  GD::sync();
-  dphase_mark(c, 6);
-  handoff_arrive();  // every input is read: group M may now change the running list, act, q, m
-  dphase_mark(c, 19);
-  // 2. per-warp metadata (lane e = entry e) and the draw / PEM-segment offsets in one warp scan
-  int nunp = 0, L = 0, base = 0, ol = 0, mcb = 0, dcnt = 0, nj = 0;
-  if (lane < n_est) {
-    nunp = S.spec_nunp[lane];
-    L = S.spec_L[lane];
-    base = S.spec_base[lane];
-    ol = S.spec_ol[lane];
-    mcb = S.spec_m[lane];
-    dcnt = nunp > Ssz ? dper : 0;  // choice() only when k = S < n (prefix_cache.py:157-158)
-    const unsigned tot = (unsigned)(nunp + L);
-    nj = tot > 0 ? (int)(((unsigned long long)(tot + (unsigned)pm.mns - 1u) * P.mns_magic) >> 32) : 0;
-  }
-  const int incl = warp_incl_scan((dcnt << 16) | nj);
-  const int jo = (incl & 0xFFFF) - nj, doff = (incl >> 16) - dcnt;
-  const int tot_incl = __shfl_sync(kFull, incl, 31);
-  const int D = tot_incl >> 16, J = tot_incl & 0xFFFF;
-  dphase_mark(c, 7);
-  if (J > kMaxJobs) {  // group-uniform: every warp computed the same totals
-    if (dt == 0) S.spec_valid = 0;
-    return;
-  }
   if (gw == 0) {
-    {
-      const unsigned nb = (unsigned)(nunp + (nunp > Ssz ? Ssz : nunp));
-      const unsigned tot_b = __reduce_add_sync(kFull, nb);
-      if (lane == 0) S.spec_alg = 4LL * tot_b;  // PEM items' + sampled tok
-    }
-    // numpy next32 positions [0, D) -> bounded draws, from the generator after this iteration's update
+    handoff_arrive();  // warp 0 reads no state group M changes from here on
+    // 1a. the numpy draws (positions [0, D) of next32, from the generator after this
+    //     iteration's update) and the sampled ratios, while warps 1.. build the summaries
+    const int D = S.spec_draws;
     const rs_pcg64_state r0 = c.rng;
     const unsigned h0 = r0.has_uint32;
     const U128 s0{r0.state_hi, r0.state_lo};
     bool rej = false;
-    {
-      const unsigned dm = __ballot_sync(kFull, lane < n_est && dcnt > 0);
-      if (lane < n_est) {
-        S.est_doff[lane] = dcnt > 0 ? doff : 0x7FFFFFFF;
-        S.est_nunp[lane] = nunp;
-        if (dcnt > 0) S.est_drawer[__popc(dm & ((1u << lane) - 1u))] = lane;
-      }
-    }
-    __syncwarp();
     const int cnt32 = D - (int)h0 > 0 ? D - (int)h0 : 0;
     const int n64 = (cnt32 + 1) >> 1;
     U128 sb = s0, s_end = s0;
-    dphase_mark(c, 8);
     uint64_t out_end = 0;
     for (int r0i = 0; r0i < n64; r0i += 32) {
       const U128 st = add128(mul128(S.jstep[lane].a, sb), S.jstep[lane].c);
@@ -652,10 +604,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
       sb.lo = __shfl_sync(kFull, st.lo, 31);
     }
     if (h0 && D > 0 && lane == 0) {  // position 0 is the buffered half-word
-      int e = 0;
-      for (int x = 0; x < n_est; ++x)
-        if (S.est_doff[x] <= 0) e = x;
-      const uint32_t bound = (uint32_t)S.est_nunp[e] - (uint32_t)Ssz;
+      const uint32_t bound = (uint32_t)S.est_nunp[S.est_drawer[0]] - (uint32_t)Ssz;
       const uint32_t excl = bound + 1u;
       const uint64_t mm = (uint64_t)r0.uinteger * excl;
       const uint32_t left = (uint32_t)mm;
@@ -669,7 +618,8 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
       if (lane == 0) S.spec_valid = 0;
     } else {
       if (lane < n_est) {  // sample_cache_miss_ratio (prefix_cache.py:141-169), utok = tok - B*m
-        const long long mh = 16LL * mcb;
+        const int nunp = S.spec_nunp[lane], base = S.spec_base[lane];
+        const long long mh = 16LL * S.spec_m[lane];
         double ratio = 0.0;
         if (nunp > 0) {
           long long usum = 0, tsum = 0;
@@ -680,7 +630,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
               tsum += t;
             }
           } else {
-            tsum = floyd_tok_sum<8>(T.tok + base, S.small.draws + doff, (uint32_t)nunp);
+            tsum = floyd_tok_sum<8>(T.tok + base, S.small.draws + S.est_doff[lane], (uint32_t)nunp);
             usum = tsum - 8 * mh;
           }
           ratio = __ddiv_rn((double)usum, (double)tsum);
@@ -703,11 +653,62 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
         S.spec_rng = r;
       }
     }
+  } else {
+    // 1b. running-row summaries after the advance (decode: gen + 1, finished rows leave)
+    for (int j = threadIdx.x - (kMWarps + 1) * 32; j < c.n_run; j += (kDWarps - 1) * 32) {
+      int e = -1, rem = 0;
+      const int a = c.run_rank[j];
+      const int g = c.run_gen[j] + (dec ? 1 : 0);
+      if (!dec || g < c.run_out[j]) {  // a decode's finished rows leave (workload.py:134-136)
+        int lo = 0, hi = n_est;          // the list is sorted by rank
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (S.spec_rank[mid] <= a) lo = mid;
+          else hi = mid;
+        }
+        e = lo;
+        rem = S.spec_ol[e] - g;
+      }
+      const unsigned act = __activemask();
+      const unsigned peers = __match_any_sync(act, e);
+      if (e >= 0) {
+        const unsigned sum = __reduce_add_sync(peers, (unsigned)rem);
+        const unsigned mx = __reduce_max_sync(peers, (unsigned)rem);
+        if (lane == __ffs(peers) - 1) {
+          atomicAdd(&S.spec_L[e], __popc(peers));
+          atomicAdd(&S.spec_rsum[e], (int)sum);
+          atomicMax(&S.spec_rmax[e], (int)mx);
+        }
+      }
+    }
+    asm volatile("bar.sync 4, %0;" ::"n"((kDWarps - 1) * 32) : "memory");  // warps 1..: summaries complete
+    handoff_arrive();  // every input is read: group M may now change the running list, act, q, m
   }
+  dphase_mark(c, 19);
+  // 2. per-warp metadata (lane e = entry e): PEM segments per entry, with the
+  //    running rows as the first segment's prefilled summary
+  int nunp = 0, L = 0, base = 0, ol = 0, nj = 0;
+  if (lane < n_est) {
+    nunp = S.spec_nunp[lane];
+    L = S.spec_L[lane];
+    base = S.spec_base[lane];
+    ol = S.spec_ol[lane];
+  }
+  int jo = 0, J = 0;
+  if (gw > 0) {
+    if (lane < n_est) {
+      const unsigned tot = (unsigned)(nunp + L);
+      nj = tot > 0 ? (int)(((unsigned long long)(tot + (unsigned)pm.mns - 1u) * P.mns_magic) >> 32) : 0;
+    }
+    const int incl = warp_incl_scan(nj);
+    jo = incl - nj;
+    J = __shfl_sync(kFull, incl, 31);
+  }
+  dphase_mark(c, 7);
   // 3. one PEM segment per warp 1..kDWarps-1; the first segment's tok loads
   //    are issued before the barrier, under the RNG replay
   for (int j = gw - 1, first = 1;; j += kDWarps - 1, first = 0) {
-    const bool act = gw > 0 && j < J;
+    const bool act = gw > 0 && j < J && J <= kMaxJobs;
     int e = 0, k = 0, ne = 0, Le = 0, basee = 0, ole = 0, t0 = 0, nloc = 0;
     int uv[8];
     if (act) {
@@ -726,6 +727,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
 #pragma unroll
     for (int i = 0; i < 8; ++i) uv[i] = (act && i < per && x0 + i < nloc) ? T.tok[basee + t0 + x0 + i] : 0;
     if (first) {
+      if (gw > 0 && lane == 0 && gw == 1) S.spec_jobs = J;
       GD::sync();
       dphase_mark(c, 20);
       dphase_mark(c, 12);
@@ -796,19 +798,36 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
     __syncwarp();
   }
+  if (gw == 0) {  // warp 0 meanwhile: the entries' segment offsets for the ordered sums
+    if (lane < n_est) {  // (the summaries are complete since the barrier above)
+      const unsigned tot = (unsigned)(nunp + S.spec_L[lane]);
+      nj = tot > 0 ? (int)(((unsigned long long)(tot + (unsigned)pm.mns - 1u) * P.mns_magic) >> 32) : 0;
+    }
+    const int incl = warp_incl_scan(nj);
+    jo = incl - nj;
+    if (lane == 0 && S.spec_jobs > kMaxJobs) S.spec_valid = 0;  // did not fit the job buffers
+  }
   GD::sync();
-  if (gw == 0 && lane < n_est) {  // ordered sums, entry by entry
   dphase_mark(c, 13);
+  if (gw == 0 && lane < n_est && S.spec_jobs <= kMaxJobs) {  // ordered sums, entry by entry, in the reference's order
     double total = 0.0;
+    int cnt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cnt[u] = u < nj ? S.small.nterm[jo + u] : 0;
     for (int j = jo; j < jo + nj; ++j) {
-      const int cnt = S.small.nterm[j];
+      const int cj = j - jo < 4 ? cnt[j - jo] : S.small.nterm[j];
       const double* tj = S.small.terms + j * kJobTerms;
+      const int nsm = cj < kJobTerms ? cj : kJobTerms;
+      int i = 0;
+      for (; i + 4 <= nsm; i += 4) {
+        const double2 x = *reinterpret_cast<const double2*>(tj + i);
+        const double2 y = *reinterpret_cast<const double2*>(tj + i + 2);
+        total = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(total, x.x), x.y), y.x), y.y);
+      }
+      for (; i < nsm; ++i) total = __dadd_rn(total, tj[i]);
       const double* spill = T.term_spill + (size_t)j * (kSmallMns + 1);
-      const int nsm = cnt < kJobTerms ? cnt : kJobTerms;
-#pragma unroll 4
-      for (int i = 0; i < nsm; ++i) total = __dadd_rn(total, tj[i]);
 #pragma unroll 1
-      for (int i = nsm; i < cnt; ++i) total = __dadd_rn(total, spill[i]);
+      for (i = nsm; i < cj; ++i) total = __dadd_rn(total, spill[i]);  // segments of > kJobTerms terms
     }
     S.spec_val[lane] = total;
   }

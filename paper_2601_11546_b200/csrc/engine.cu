@@ -1304,7 +1304,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
                         8 * (size_t)(R + 1) + 8 * (size_t)R + 8 * (size_t)(R + 1) + 4 * (size_t)R +
                         rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
                         (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
-                        12 * (size_t)(R + 1) + 8 + 36 * 256;
+                        12 * (size_t)(R + 1) + 8 + 24 * (size_t)R /* static-order sort scratch */ + 40 * 256;
     TRY(arena_reserve(h, need));
     if (N < (1LL << 16)) {  // small trace: compose the arena on the host, upload it in two copies
       h.staging = true;

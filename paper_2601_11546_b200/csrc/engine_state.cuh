@@ -240,6 +240,8 @@ struct Shared {
   double spec_val[kSmallEst];
   rs_pcg64_state spec_rng;
   long long spec_alg;
+  int spec_draws;  // next32 values the speculative update draws
+  int spec_jobs;   // its PEM segments
   // batched prefill eviction
   int fp_bad, fp_popped, fp_par, fp_cut;
   long long fp_rem;
@@ -256,7 +258,7 @@ struct Shared {
     struct {  // side by side: the pipelined iteration runs the DPU fast path and the prefill advance at once
       struct {
         unsigned int draws[kSmallEst * 31];
-        double terms[kMaxJobs * kJobTerms];
+        alignas(16) double terms[kMaxJobs * kJobTerms];  // read two at a time by the ordered sums
         int nterm[kMaxJobs];
         int U[kWarps][kSmallMns];  // per-warp utok prefix of the segment it evaluates
       } small;
