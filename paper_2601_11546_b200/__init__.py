@@ -36,7 +36,7 @@ from .priority import (
     static_relquery_prio,
     static_req_prio,
 )
-from .report import decompose
+from .report import SummaryTable, decompose, summarize
 from .workload import (
     OUTPUT_LIMITS,
     ArrivalTrace,
@@ -58,5 +58,5 @@ __all__ = [
     "TimestampLedger", "TraceColumns", "TraceConfig", "WORLD_PRESETS", "generate_heavy_tail_trace",
     "generate_trace", "load_model", "load_trace", "pem", "pem_batch", "predict_decode", "predict_prefill",
     "remainder_items", "run", "save_model", "save_trace", "static_relquery_prio", "static_req_prio",
-    "world_preset",
+    "summarize", "SummaryTable", "world_preset",
 ]

@@ -101,31 +101,35 @@ class RunResult:
         return (self.dpu_wall_s + self.aba_wall_s) / self.sim_duration
 
     def write_relquery_csv(self, path) -> None:
+        """Per-relQuery latency breakdown in rel_id order, floats as repr (engine.py:104-125)."""
         import csv
         from pathlib import Path
 
         from .report import decompose
 
-        with Path(path).open("w", newline="") as f:
-            w = csv.writer(f)
-            w.writerow(["rel_id", "size", "arrival_s", "waiting_s", "core_s", "tail_s", "total_s"])
+        def rows():
             for rel_id in sorted(self.ledgers):
                 led = self.ledgers[rel_id]
                 b = decompose(rel_id, led)
-                w.writerow([rel_id, self.relquery_sizes[rel_id], repr(led.arrival), repr(b.waiting_s),
-                            repr(b.core_s), repr(b.tail_s), repr(b.total_s)])
+                yield [rel_id, self.relquery_sizes[rel_id],
+                       *map(repr, (led.arrival, b.waiting_s, b.core_s, b.tail_s, b.total_s))]
+
+        with Path(path).open("w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["rel_id", "size", "arrival_s", "waiting_s", "core_s", "tail_s", "total_s"])
+            w.writerows(rows())
 
     def write_decision_csv(self, path) -> None:
+        """One row per logged iteration; None fields empty (engine.py:127-138)."""
         import csv
         from pathlib import Path
 
         with Path(path).open("w", newline="") as f:
             w = csv.writer(f)
-            w.writerow(["iteration", "clock_s", "case", "m_plus", "m_minus",
-                        "delta_plus", "delta_minus", "delta_total", "action"])
-            for e in self.decision_log:
-                w.writerow([e.iteration, repr(e.clock), e.case, e.m_plus, e.m_minus,
-                            e.delta_plus, e.delta_minus, e.delta_total, e.action])
+            w.writerow(["iteration", "clock_s", "case", "m_plus", "m_minus", "delta_plus", "delta_minus",
+                        "delta_total", "action"])
+            w.writerows([e.iteration, repr(e.clock), e.case, e.m_plus, e.m_minus, e.delta_plus, e.delta_minus,
+                         e.delta_total, e.action] for e in self.decision_log)
 
 
 @dataclass

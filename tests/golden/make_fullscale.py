@@ -24,7 +24,7 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from fullscale_util import RUNS, WORKLOADS, fingerprint  # noqa: E402
+from fullscale_util import RUNS, WINDOWS, WORKLOADS, fingerprint  # noqa: E402
 
 
 def main():
@@ -47,6 +47,25 @@ def main():
                    "cache_hit_tokens": int(r.cache_hit_tokens), "cache_miss_tokens": int(r.cache_miss_tokens),
                    "oracle_wall_s": round(wall, 1), "workload": wl, "policy": policy})
         out["configs"][name] = fp
+        print(name, r.iterations, f"{wall:.1f} s", flush=True)
+        path.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
+    from dataclasses import replace
+
+    for name, (wl, policy, n) in WINDOWS.items():
+        if only and name not in only:
+            continue
+        trace, world, cfg = WORKLOADS[wl]()
+        t0 = time.perf_counter()
+        r = oracle.run(trace, policy, world, replace(cfg, iteration_limit=n), None, 0)
+        wall = time.perf_counter() - t0
+        assert r.status == 3 and r.iterations == n, (r.status, r.iterations, r.message)  # SimulationAborted at n
+        fp = fingerprint(r.log, r.completion_iter)
+        fp.update({"iterations": int(r.iterations), "clock": repr(float(r.clock)),
+                   "cache_hit_tokens": int(r.cache_hit_tokens), "cache_miss_tokens": int(r.cache_miss_tokens),
+                   "kv_reserved": int(r.kv_reserved), "oracle_wall_s": round(wall, 1), "workload": wl,
+                   "policy": policy, "window": n})
+        out["windows"] = out.get("windows", {})
+        out["windows"][name] = fp
         print(name, r.iterations, f"{wall:.1f} s", flush=True)
         path.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
 

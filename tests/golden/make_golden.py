@@ -183,7 +183,15 @@ def model_of(m):
     return LinearCostModel(*m)
 
 
-def run_case(name, spec, policy, world, config=None, policy_model=None, seed=0, window=None, full=True):
+def _csv_text(write) -> str:
+    with tempfile.TemporaryDirectory() as d:
+        p = Path(d) / "out.csv"
+        write(p)
+        return p.read_text()
+
+
+def run_case(name, spec, policy, world, config=None, policy_model=None, seed=0, window=None, full=True,
+             csv=False):
     t0 = time.perf_counter()
     trace = ref_trace(spec)
     t_gen = time.perf_counter() - t0
@@ -241,6 +249,8 @@ def run_case(name, spec, policy, world, config=None, policy_model=None, seed=0, 
         "iters": eng.rec,
         "timing": {"trace_s": t_gen, "run_s": t_run},
     }
+    if csv and res is not None:  # RunResult CSVs (engine.py:104-138), byte for byte
+        out["csv"] = {"relquery": _csv_text(res.write_relquery_csv), "decision": _csv_text(res.write_decision_csv)}
     p = GOLDEN_DIR / f"{name}.json.gz"
     with gzip.open(p, "wt", compresslevel=9) as f:
         json.dump(out, f, separators=(",", ":"))
@@ -259,11 +269,11 @@ TIGHT = {"constraints": [4000, 16, 512]}
 
 CASES = {
     # config 1: all five policies
-    "cfg1_relserve": dict(spec=CFG1, policy="relserve", world="opt-13b-like"),
-    "cfg1_fcfs": dict(spec=CFG1, policy="fcfs", world="opt-13b-like"),
-    "cfg1_sp": dict(spec=CFG1, policy="sp", world="opt-13b-like"),
-    "cfg1_pp": dict(spec=CFG1, policy="relserve-pp", world="opt-13b-like"),
-    "cfg1_dp": dict(spec=CFG1, policy="relserve-dp", world="opt-13b-like"),
+    "cfg1_relserve": dict(spec=CFG1, csv=True, policy="relserve", world="opt-13b-like"),
+    "cfg1_fcfs": dict(spec=CFG1, csv=True, policy="fcfs", world="opt-13b-like"),
+    "cfg1_sp": dict(spec=CFG1, csv=True, policy="sp", world="opt-13b-like"),
+    "cfg1_pp": dict(spec=CFG1, csv=True, policy="relserve-pp", world="opt-13b-like"),
+    "cfg1_dp": dict(spec=CFG1, csv=True, policy="relserve-dp", world="opt-13b-like"),
     # sp with user priority functions of either sign (priority.py:221-235)
     "sp_negative": dict(spec=gen({"num_relqueries": 30, "size_range": [1, 40], "rate": 4.0, "seed": 41}),
                         policy="sp", world="opt-13b-like", config={"sp_fns": "neg_mixed"}),
@@ -286,7 +296,7 @@ CASES = {
                          config={"capacity_blocks": 100, "block_size": 8, "sample_size": 3}),
     # starvation override
     "tau_relserve": dict(spec=gen({"num_relqueries": 40, "size_range": [1, 60], "rate": 2.0, "seed": 11}),
-                         policy="relserve", world=list(TEST_MODEL), config={"tau": 0.05}),
+                         policy="relserve", world=list(TEST_MODEL), config={"tau": 0.05}, csv=True),
     "starve_tau": dict(spec=STARVE, policy="relserve", world=list(TEST_MODEL), config={"tau": 0.05}),
     "starve_inf": dict(spec=STARVE, policy="relserve", world=list(TEST_MODEL)),
     "hol_relserve": dict(spec=HOL, policy="relserve", world=list(TEST_MODEL)),
@@ -319,8 +329,40 @@ CASES = {
 }
 
 
+#: report.summarize (report.py:101-155) over full reference runs: (trace spec, policy, world) each;
+#: config 1 at two rates under every policy, so speedups vs fcfs exist at both rates
+SUMMARY_RUNS = [(gen({"num_relqueries": 8, "size_range": [100, 100], "rate": r, "seed": 0}), p, "opt-13b-like")
+                for r in (1.0, 2.0) for p in ("fcfs", "sp", "relserve", "relserve-pp", "relserve-dp")]
+
+
+def make_summary():
+    """tests/golden/summary.json: the summary tables' CSV bytes (wide and long, baselines fcfs
+    and sp) and each run's ledgers and sizes, for the report parity tests."""
+    from relsim.report import summarize
+
+    runs, rows = [], []
+    for spec, policy, world in SUMMARY_RUNS:
+        res = Engine(ref_trace(spec), policy, model_of(world), EngineConfig(), None, 0).run()
+        runs.append(res)
+        rows.append({"spec": spec, "policy": policy, "world": world, "rate": res.rate,
+                     "ledgers": [[k, v.arrival, v.first_prefill_start, v.last_prefill_end, v.last_decode_end]
+                                 for k, v in res.ledgers.items()],
+                     "sizes": [[k, v] for k, v in res.relquery_sizes.items()]})
+    out = {"numpy": np.__version__, "reference": "relsim " + getattr(relsim, "__version__", "?"), "runs": rows,
+           "tables": {}}
+    for base in ("fcfs", "sp"):
+        t = summarize(runs, baseline=base)
+        out["tables"][base] = {"wide": _csv_text(t.write_csv), "long": _csv_text(t.write_long_csv)}
+    p = GOLDEN_DIR / "summary.json"
+    p.write_text(json.dumps(out, indent=1) + "\n")
+    print(f"summary: {len(runs)} runs -> {p.stat().st_size} B")
+
+
 def main(argv):
     GOLDEN_DIR.mkdir(parents=True, exist_ok=True)
+    if argv == ["summary"]:
+        make_summary()
+        return
     names = argv or [n for n in CASES if not n.startswith(("cfg2", "cfg3"))]
     for n in names:
         run_case(n, **CASES[n])

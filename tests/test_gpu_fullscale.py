@@ -17,8 +17,10 @@ Configs 2 and 3 under every policy are also compared bit for bit with the CPU or
 through fingerprints: SHA-256 per decision-record field and of the per-request
 completion iterations, exact final clock and cache counters
 (tests/golden/fullscale.json, made by tests/golden/make_fullscale.py).  The
-config-5 pool (≈ 80 oracle iterations/s) is checked against the unsharded device
-run instead, whose configs 2/3 counterparts are the oracle-pinned ones.
+config-5 pool (≈ 80 oracle iterations/s) is compared with the oracle over its
+first 3,000 iterations at full size (first sight of all 40,000 relQueries
+included), unsharded and sharded 8 ways; its complete run is checked against the
+unsharded device run.
 """
 
 import json
@@ -92,7 +94,9 @@ def _check_run(res, trace, cfg):
     assert res.sim_duration == last
 
 
-_GOLDEN = json.loads((Path(__file__).parent / "golden" / "fullscale.json").read_text())["configs"]
+_FULL = json.loads((Path(__file__).parent / "golden" / "fullscale.json").read_text())
+_GOLDEN = _FULL["configs"]
+_WINDOWS = _FULL.get("windows", {})
 
 
 @pytest.mark.parametrize("name", sorted(_GOLDEN))
@@ -122,3 +126,33 @@ def test_config5_sharded_full_run_equals_unsharded():
     assert np.array_equal(a.completion_iteration, b.completion_iteration)
     assert (a.cache_hit_tokens, a.cache_miss_tokens) == (b.cache_hit_tokens, b.cache_miss_tokens)
     _check_run(b, trace, cfg)
+
+
+@pytest.mark.parametrize("shards", [1, 8])
+@pytest.mark.parametrize("name", sorted(_WINDOWS))
+def test_full_size_window_equals_oracle(name, shards):
+    """Config 5 at full size (8e6 requests in one pool), the first 3,000 iterations: the
+    device run -- unsharded, and sharded 8 ways with the per-iteration exchange -- equals the
+    oracle's, record for record (SHA-256 per decision field, per-request completion
+    iterations), with the same clock, cache counters and kv at the window's end."""
+    from dataclasses import replace
+
+    from fullscale_util import WINDOWS, WORKLOADS, fingerprint
+    from paper_2601_11546_b200.engine import Engine, SimulationAborted
+
+    wl, policy, n = WINDOWS[name]
+    trace, world, cfg = WORKLOADS[wl]()
+    eng = Engine(trace, policy, world, replace(cfg, iteration_limit=n), None, 0, device=0, shards=shards)
+    with pytest.raises(SimulationAborted):
+        eng.run()
+    res = eng.result
+    st = eng._status
+    eng.close()
+    g = _WINDOWS[name]
+    assert res.iterations == g["iterations"] == n
+    assert repr(float(res.sim_duration)) == g["clock"]
+    assert (res.cache_hit_tokens, res.cache_miss_tokens) == (g["cache_hit_tokens"], g["cache_miss_tokens"])
+    assert int(st.kv_reserved) == g["kv_reserved"]
+    fp = fingerprint(res.records, res.completion_iteration.astype(np.int64))
+    for k, v in fp.items():
+        assert v == g[k], k
