@@ -105,8 +105,11 @@ __device__ int cache_evict(Ctl& c, const TraceDev& T, const RqView& rq, long lon
 __device__ long long prefill_row_cache(Ctl& c, const TraceDev& T, const RqView& rq, const Params& P, int a,
                                        int tok) {
   const long long B = P.cfg.block_size;
-  const int nb = (int)(tok / B);
-  const int Pc = rq.chain[a];
+  const long long C = P.cfg.capacity_blocks;
+  // a sequence longer than the whole cache inserts only its first C blocks
+  // (prefix_cache.py:101-103, last_insert_truncated)
+  const int nb = (int)(tok / B < C ? tok / B : C);
+  const int Pc = rq.chain[a] < nb ? rq.chain[a] : nb;
   const int T_len = nb - Pc;
   const int mb = rq.m[a];
   const long long hit = B * mb;
@@ -231,7 +234,8 @@ __device__ bool prefill_fast(const Params& P, const TraceDev& T, Shared& S, int 
         tk = tokv[i];
         tl = (int)(tk / B) - Pc;
       }
-      int v[3] = {tl, tk, (i < n && tl <= 0) ? 1 : 0}, tot[3];
+      // rows without a private tail, or truncated by the capacity: the exact path
+      int v[3] = {tl, tk, (i < n && (tl <= 0 || tk / B > C)) ? 1 : 0}, tot[3];
       group_scan32<G, 3>(v, S.s32, tot, tid >> 5);
       Tv[s] = tl;
       inclT[s] = cT + v[0];

@@ -919,6 +919,85 @@ __global__ void __launch_bounds__(kThreads) first_sight_kernel(int R, const int*
   }
 }
 
+// First sight, segment-parallel (when PEM segments close by count only,
+// mns <= 256): one warp per PEM segment of every relQuery -- a whole-grid,
+// bandwidth-shaped pass that reads each row's tok once -- writes the
+// segment's terms in the reference's order (its prefill sub-batches, then the
+// decode term: pem(), priority.py:187-217, every row unprefilled with utok =
+// tok and remaining = output_limit); first_sight_sum_kernel then adds each
+// relQuery's terms in order.  seg_pref[a] = the first segment of relQuery a.
+// Terms per segment are bounded by 2*sum(tok)/mnbt + 3 (consecutive next-fit
+// sub-batches exceed mnbt together); the host sizes `bound` from max(tok).
+__global__ void __launch_bounds__(kThreads) first_sight_seg_kernel(int R, int n_seg, const int* off, const int* ol,
+                                                                   const int* seg_pref, const int* tok, PemModel m,
+                                                                   int bound, double* terms, int* nterm) {
+  __shared__ int U[kWarps][kSmallMns];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mns = (int)m.mns;
+  int* Uw = U[warp];
+  for (int sg = blockIdx.x * kWarps + warp; sg < n_seg; sg += gridDim.x * kWarps) {
+    int lo = 0, hi = R;  // the relQuery: the last a with seg_pref[a] <= sg
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (seg_pref[mid] <= sg) lo = mid;
+      else hi = mid;
+    }
+    const int a = lo, k = sg - seg_pref[a];
+    const int r0 = off[a] + k * mns, r1 = min(off[a + 1], r0 + mns), nloc = r1 - r0;
+    const int per = (nloc + 31) >> 5, x0 = lane * per;  // per <= 8
+    int uv[8], ls = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uv[i] = (i < per && x0 + i < nloc) ? tok[r0 + x0 + i] : 0;
+      ls += uv[i];
+    }
+    int run = warp_incl_scan(ls) - ls;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      run += uv[i];
+      if (i < per && x0 + i < nloc) Uw[x0 + i] = run;
+    }
+    __syncwarp();
+    double* tj = terms + (size_t)sg * bound;
+    int nt = 0, bb = 0;
+    while (bb < nloc) {  // the prefill sub-batch chain (see dpu_small)
+      const int before = bb ? Uw[bb - 1] : 0;
+      const int ub = Uw[bb];
+      const int thr = ub - before > m.mnbt ? ub : before + (int)m.mnbt;
+      int nb = nloc;
+      for (int b2 = bb + 1; b2 < nloc; b2 += 32) {
+        const unsigned mx = __ballot_sync(kFull, b2 + lane < nloc && Uw[b2 + lane] > thr);
+        if (mx) {
+          nb = b2 + __ffs(mx) - 1;
+          break;
+        }
+      }
+      if (lane == 0) tj[nt] = lin(m.ap, (double)(Uw[nb - 1] - before), m.bp);
+      ++nt;
+      bb = nb;
+    }
+    if (lane == 0) {
+      const long long o = ol[a];
+      tj[nt] = __dadd_rn(__dmul_rn(m.ad, (double)((long long)nloc * o)), __dmul_rn(m.bd, (double)o));
+      nterm[sg] = nt + 1;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void first_sight_sum_kernel(int R, const int* seg_pref, int bound, const double* terms, const int* nterm,
+                                       double* out) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < R; a += gridDim.x * blockDim.x) {
+    double total = 0.0;  // pem() accumulates its terms in scan order (priority.py:197-218)
+    for (int sg = seg_pref[a]; sg < seg_pref[a + 1]; ++sg) {
+      const double* tj = terms + (size_t)sg * bound;
+      const int nt = nterm[sg];
+      for (int i = 0; i < nt; ++i) total = __dadd_rn(total, tj[i]);
+    }
+    out[a] = total;
+  }
+}
+
 // Engine-creation row checks (engine.py:235-239 and the device model's limits),
 // one warp per relQuery over the uploaded rows: res[0] = the first admission
 // rank with an offending row (INT_MAX if none), res[1] = the largest tok.  The
@@ -1470,8 +1549,6 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       max_tok_all = res[1];
       max_nb = max_tok_all / cfg->block_size;
     }
-    if (max_nb > cfg->capacity_blocks)
-      return fail(RS_EUNSUPPORTED, "a request has more whole blocks than the cache capacity (truncated insert)");
     {
       const long long max_tok = max_tok_all;
       d.seg_ok = cfg->max_num_seqs * max_tok <= cfg->cap && max_tok * kItemBuf < (1LL << 31);
@@ -1486,11 +1563,48 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       if (!d_ol) TRY(dalloc(h, &d_ol, R, ol.data()));
       PemModel m{h.pol.alpha_p, h.pol.beta_p, h.pol.alpha_d, h.pol.beta_d, cfg->cap, cfg->max_num_seqs,
                  cfg->max_num_batched_tokens};
-      const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
-      TRY(stage_flush(h));  // the kernel reads the rows and writes fsprio
-      first_sight_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d.tok, m, (double*)d.fsprio);
+      // segment-parallel when segments close by count only and their terms are few
+      const long long bound = 2 * cfg->max_num_seqs * max_tok_all / cfg->max_num_batched_tokens + 3;
+      const bool seg_fs = d.seg_ok && cfg->max_num_seqs <= kSmallMns && bound <= 64;
+      std::vector<int> segp;
+      if (seg_fs) {
+        segp.assign(R + 1, 0);
+        for (long long a = 0; a < R; ++a) {
+          const long long sz = off[a + 1] - off[a];
+          segp[a + 1] = segp[a] + (int)((sz + cfg->max_num_seqs - 1) / cfg->max_num_seqs);
+        }
+      }
+      int *d_segp = nullptr, *d_nt = nullptr;
+      double* d_terms = nullptr;
+      void* scratch = nullptr;  // stream-ordered pool scratch, freed after the kernels
+      if (seg_fs) {
+        const size_t ns = (size_t)std::max(segp[R], 1);
+        const size_t b_terms = ns * bound * sizeof(double), b_nt = (ns * 4 + 255) & ~(size_t)255;
+        const size_t b_segp = ((size_t)(R + 1) * 4 + 255) & ~(size_t)255;
+        if (cudaMallocAsync(&scratch, b_terms + b_nt + b_segp, 0) != cudaSuccess)
+          return fail(RS_ENOMEM, "first-sight scratch");
+        d_terms = (double*)scratch;
+        d_nt = (int*)((char*)scratch + b_terms);
+        d_segp = (int*)((char*)scratch + b_terms + b_nt);
+        if (cudaMemcpyAsync(d_segp, segp.data(), (size_t)(R + 1) * 4, cudaMemcpyHostToDevice, 0) != cudaSuccess)
+          return fail(RS_ECUDA, "first-sight segment upload");
+      }
+      TRY(stage_flush(h));  // the kernels read the rows and write fsprio
+      if (seg_fs) {
+        const int ns = segp[R];
+        const int grid = (int)std::min<long long>((ns + kWarps - 1) / kWarps, 148 * 4);
+        if (ns > 0)
+          first_sight_seg_kernel<<<grid, kThreads>>>((int)R, ns, d_off, d_ol, d_segp, d.tok, m, (int)bound, d_terms,
+                                                     d_nt);
+        first_sight_sum_kernel<<<(unsigned)std::min<long long>((R + 255) / 256, 148 * 4), 256>>>(
+            (int)R, d_segp, (int)bound, d_terms, d_nt, (double*)d.fsprio);
+        cudaFreeAsync(scratch, 0);
+      } else {
+        const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
+        first_sight_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d.tok, m, (double*)d.fsprio);
+      }
       const cudaError_t ke = cudaGetLastError();  // stream-ordered before the static-order sort below
-      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first_sight_kernel: ") + cudaGetErrorString(ke));
+      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first-sight kernels: ") + cudaGetErrorString(ke));
     }
   }
   pc.mark("first-sight kernel");

@@ -73,16 +73,31 @@ __device__ __forceinline__ void sort_scatter(const unsigned long long* sk, const
     const unsigned rank = __popc(peers & lt);
     if (in && rank == 0) sm.wcnt[warp][d] = __popc(peers);
     __syncthreads();
-    // per digit: exclusive scan over the warps, from the digit's running base
-    for (int b = threadIdx.x; b < 256; b += kSortThreads) {
-      unsigned run = sm.base[b];
-#pragma unroll 8
-      for (int w = 0; w < kSortWarps; ++w) {
-        const unsigned t = sm.wcnt[w][b];
-        sm.wcnt[w][b] = run;
-        run += t;
+    // per digit: exclusive scan over the warps, from the digit's running base --
+    // four threads per digit (the same warp), eight warps' counts each
+    {
+      static_assert(kSortThreads == 4 * 256 && kSortWarps == 32, "4 threads x 8 warps per digit");
+      const int d = threadIdx.x >> 2, part = threadIdx.x & 3;
+      unsigned c8[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        c8[i] = sm.wcnt[part * 8 + i][d];
+        sum += c8[i];
       }
-      sm.base[b] = run;
+      unsigned incl = sum;
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        const unsigned x = __shfl_up_sync(0xFFFFFFFFu, incl, o, 4);
+        if (part >= o) incl += x;
+      }
+      unsigned run = sm.base[d] + incl - sum;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        sm.wcnt[part * 8 + i][d] = run;
+        run += c8[i];
+      }
+      __syncwarp();
+      if (part == 3) sm.base[d] = run;  // every part has read the base
     }
     __syncthreads();
     if (in) {

@@ -294,6 +294,12 @@ CASES = {
                                    "mean_input_len": 90}),
                          policy="relserve-pp", world="opt-13b-like",
                          config={"capacity_blocks": 100, "block_size": 8, "sample_size": 3}),
+    # truncated inserts: rows with more whole blocks than the whole cache (prefix_cache.py:101-103)
+    "evict_truncate": dict(spec=gen({"num_relqueries": 20, "size_range": [1, 20], "rate": 3.0, "seed": 29}),
+                           policy="relserve", world="opt-13b-like", config={"capacity_blocks": 10}),
+    "evict_truncate_fcfs": dict(spec=gen({"num_relqueries": 15, "size_range": [1, 12], "rate": 5.0, "seed": 30,
+                                          "mean_input_len": 300}),
+                                policy="fcfs", world="opt-13b-like", config={"capacity_blocks": 14}),
     # starvation override
     "tau_relserve": dict(spec=gen({"num_relqueries": 40, "size_range": [1, 60], "rate": 2.0, "seed": 11}),
                          policy="relserve", world=list(TEST_MODEL), config={"tau": 0.05}, csv=True),
