@@ -234,6 +234,16 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
                             int64_t* completion_iter, double* priority);
 
 /*
+ * Every trace's results at once (multi-trace engines, e.g. a sweep of
+ * independent traces): the ledgers' first_prefill_start / last_prefill_end /
+ * last_decode_end (NaN = None) of all relQueries and the completion iteration
+ * of all requests, traces concatenated in creation order, each in trace order
+ * -- one page-locked batch of copies on `stream` and one synchronisation.
+ * Any output pointer may be NULL.
+ */
+int rs_engine_read_results(rs_engine* e, void* stream, double* first_prefill_start, double* last_prefill_end,
+                           double* last_decode_end, int32_t* completion_iter);
+/*
  * Completion iteration per request (trace order, -1 = not finished) as int32:
  * the device column copied straight into `completion_iter` (page-locked
  * memory makes it one DMA).  The per-request output the reference's ledgers

@@ -100,6 +100,8 @@ def lib():
     L.rs_engine_read_dpu.restype = C.c_int
     L.rs_engine_read_dpu.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p]
+    L.rs_engine_read_results.restype = C.c_int
+    L.rs_engine_read_results.argtypes = [C.c_void_p, C.c_void_p] + [C.c_void_p] * 4
     L.rs_sort_pairs.restype = C.c_int
     L.rs_sort_pairs.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32]
     _lib = L
@@ -113,7 +115,7 @@ EXPORTED_SYMBOLS = (
     "rs_engine_destroy", "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
     "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange", "rs_waiting_argmin",
-    "rs_engine_read_order", "rs_engine_read_dpu", "rs_sort_pairs", "rs_trace_v1_load", "rs_trace_v1_info", "rs_trace_v1_columns", "rs_trace_v1_free",
+    "rs_engine_read_order", "rs_engine_read_dpu", "rs_sort_pairs", "rs_engine_read_results", "rs_trace_v1_load", "rs_trace_v1_info", "rs_trace_v1_columns", "rs_trace_v1_free",
     "rs_trace_v1_error",
 )
 
@@ -232,6 +234,15 @@ class NativeEngine:
         if count:
             _check(lib().rs_engine_read_dpu(self.h, t, first, count, vals.ctypes.data, flags.ctypes.data, rng))
         return vals[:, :R], flags[:, :R], [rng[i] for i in range(count)]
+
+    def read_results(self, R_total: int, N_total: int, stream=None):
+        """Every trace's ledgers (first_prefill_start, last_prefill_end, last_decode_end) and
+        completion iterations, traces concatenated (include/relserve.h rs_engine_read_results)."""
+        b, c, d = (np.zeros(R_total, np.float64) for _ in range(3))
+        comp = np.zeros(N_total, np.int32)
+        _check(lib().rs_engine_read_results(self.h, _stream_ptr(stream), b.ctypes.data, c.ctypes.data,
+                                            d.ctypes.data, comp.ctypes.data))
+        return b, c, d, comp
 
     def read_ledgers(self, t: int, R: int):
         a, b, c, d = (np.zeros(R, np.float64) for _ in range(4))

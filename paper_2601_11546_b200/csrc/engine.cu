@@ -30,6 +30,8 @@
 #include <chrono>
 #include <cstddef>
 #include <cstdlib>
+#include <functional>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -1107,6 +1109,7 @@ struct HostTrace {
   char* arena = nullptr;
   void* arena_alloc = nullptr;  // cudaMallocAsync (pool) allocation
   size_t arena_cap = 0, arena_used = 0;
+  size_t arena_top = 0;  // staging: buffers needing no initialisation are carved from the top (never uploaded)
   double* noise_buf = nullptr;  // rs_engine_set_noise
   // small traces: arena contents are composed in a host image and uploaded in
   // one copy per flush (stage_flush) instead of a copy / memset per buffer
@@ -1114,7 +1117,23 @@ struct HostTrace {
   std::vector<unsigned char> stage;
   size_t staged_lo = 0;  // arena bytes [staged_lo, arena_used) not uploaded yet
   std::vector<int> zorder;      // every relQuery in the static waiting order
+  bool no_log = false;          // created with log_capacity 0 (the device writes a scratch record)
+  // small traces: the staged arena image and the creation kernels wait for one
+  // engine-wide upload (finish_deferred)
+  bool deferred = false;
+  std::vector<std::function<int()>> pending;  // kernel launches after the upload, in order
 };
+
+// Page-locked staging for the deferred uploads of engine creation, reused
+// across engines (allocating page-locked memory costs far more than the copy);
+// a reuse waits for the previous creation's copies (an event).
+struct PinnedStage {
+  std::mutex mu;
+  unsigned char* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+};
+PinnedStage g_pinned;
 
 // Reserve the trace's arena: every dalloc below carves from it (256-byte aligned).
 // The arena comes from the device's stream-ordered pool, which keeps freed
@@ -1134,11 +1153,13 @@ void keep_pool(int device) {
 
 int arena_reserve(HostTrace& h, size_t bytes) {
   void* q = nullptr;
+  bytes = (bytes + 255) & ~(size_t)255;  // both ends of the arena carve 256-byte aligned buffers
   cudaError_t e = cudaMallocAsync(&q, bytes, 0);
   if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
   h.arena_alloc = q;
   h.arena = (char*)q;
   h.arena_cap = bytes;
+  h.arena_top = bytes;
   h.arena_used = 0;
   return RS_OK;
 }
@@ -1157,7 +1178,15 @@ int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_by
   if (n == 0) n = 1;
   void* q = nullptr;
   const size_t nb = (n * sizeof(T) + 255) & ~(size_t)255;
-  if (h.staging && h.arena && h.arena_used + nb <= h.arena_cap && !src && fill_byte >= 0 && nb >= (64u << 10)) {
+  if (h.staging && h.arena && !src && fill_byte < 0 && h.arena_used + nb <= h.arena_top) {
+    // no contents: from the top of the arena, outside the uploaded image
+    h.arena_top -= nb;
+    h.bytes += (long long)(n * sizeof(T));
+    *p = (T*)(h.arena + h.arena_top);
+    return RS_OK;
+  }
+  if (h.staging && !h.deferred && h.arena && h.arena_used + nb <= h.arena_top && !src && fill_byte >= 0 &&
+      nb >= (64u << 10)) {
     // a large fill (the decision-log ring): flush what is composed, fill on the device
     int rc = stage_flush(h);
     if (rc) return rc;
@@ -1170,16 +1199,17 @@ int dalloc(HostTrace& h, T** p, size_t n, const void* src = nullptr, int fill_by
     *p = (T*)q;
     return RS_OK;
   }
-  if (h.staging && h.arena && h.arena_used + nb <= h.arena_cap) {  // composed on the host
+  if (h.staging && h.arena && h.arena_used + nb <= h.arena_top) {  // composed on the host
     const size_t at = h.arena_used;
     h.arena_used += nb;
     h.bytes += (long long)(n * sizeof(T));
+    h.stage.resize(h.arena_used);  // grows with the image (capacity reserved up front)
     if (src) memcpy(h.stage.data() + at, src, n * sizeof(T));
     else if (fill_byte >= 0) memset(h.stage.data() + at, fill_byte, n * sizeof(T));
     *p = (T*)(h.arena + at);
     return RS_OK;
   }
-  if (h.arena && h.arena_used + nb <= h.arena_cap) {
+  if (h.arena && h.arena_used + nb <= h.arena_top) {
     q = h.arena + h.arena_used;
     h.arena_used += nb;
   } else {
@@ -1287,6 +1317,7 @@ struct rs_engine {
   TraceDev* d_traces = nullptr;
   size_t smem = 0;
   cudaEvent_t done = nullptr;  // recorded after every launch: destroy waits on it before the stream-ordered frees
+  cudaEvent_t ready = nullptr;  // creation's asynchronous uploads and kernels (legacy stream) are complete
 };
 
 extern "C" {
@@ -1314,6 +1345,21 @@ static int validate_config(const rs_config* cfg) {
     return fail(RS_EUNSUPPORTED, "sample_size above the device limit (64)");
   if (cfg->max_num_seqs > kMaxRun) return fail(RS_EUNSUPPORTED, "max_num_seqs above the device limit (1024)");
   return RS_OK;
+}
+
+// Upper bound of one trace's arena (build_trace's buffers, 256-byte aligned each).
+static size_t arena_need(const rs_trace_view& v, const rs_config* cfg, long long log_cap) {
+  const size_t R = (size_t)std::max<long long>(v.num_relqueries, 0), N = (size_t)std::max<long long>(v.num_requests, 0);
+  long long fifo_cap = 1;
+  while (fifo_cap < cfg->capacity_blocks + kMaxRun + 2) fifo_cap <<= 1;
+  long long lc = 1;  // a one-record ring when no log is kept
+  while (lc < log_cap) lc <<= 1;
+  const size_t need = 16 * N + 24 * R + 8 * (size_t)kMaxJobs * (kSmallMns + 1) + 8 * (R + 1) + 8 * R + 8 * (R + 1) +
+                      4 * R + rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
+                      (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
+                      12 * (R + 1) + 8 + 24 * R /* static-order sort scratch */ +
+                      4 * (R + 1) /* first-sight segments */ + 44 * 256;
+  return (need + 255) & ~(size_t)255;
 }
 
 static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_cost_model& pol,
@@ -1372,22 +1418,18 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
 #define TRY(x) \
   if ((rc = (x))) return rc
   {  // arena: an upper bound of every buffer below (+256 B alignment slack each)
-    long long fifo_cap = 1;
-    while (fifo_cap < cfg->capacity_blocks + kMaxRun + 2) fifo_cap <<= 1;
-    long long lc = 0;
-    if (log_cap > 0) {
-      lc = 1;
-      while (lc < log_cap) lc <<= 1;
+    const size_t need = arena_need(v, cfg, log_cap);
+    if (h.arena_cap >= need) {  // a slice of the engine-wide arena (create_impl)
+      h.arena_top = h.arena_cap;
+      h.arena_used = 0;
+    } else {
+      TRY(arena_reserve(h, need));
     }
-    const size_t need = 16 * (size_t)N + 24 * (size_t)R + 8 * (size_t)kMaxJobs * (kSmallMns + 1) +
-                        8 * (size_t)(R + 1) + 8 * (size_t)R + 8 * (size_t)(R + 1) + 4 * (size_t)R +
-                        rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
-                        (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
-                        12 * (size_t)(R + 1) + 8 + 24 * (size_t)R /* static-order sort scratch */ + 40 * 256;
-    TRY(arena_reserve(h, need));
-    if (N < (1LL << 16)) {  // small trace: compose the arena on the host, upload it in two copies
+    if (N < (1LL << 16)) {  // small trace: compose the arena on the host, upload it with the others at the end
       h.staging = true;
-      h.stage.assign(need, 0);
+      h.deferred = shard_world == 1;
+      h.stage.clear();
+      h.stage.reserve(need);
       h.staged_lo = 0;
     }
   }
@@ -1522,7 +1564,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   TRY(dalloc(h, &d.lde, R, nullptr, 0xFF));
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
-  TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
+  TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1)));  // scratch: written before read
   {
     std::vector<int> nep(R + 1, 0);  // relQueries with rows among admission ranks [0, a)
     for (long long a = 0; a < R; ++a) nep[a + 1] = nep[a] + (off[a + 1] > off[a]);
@@ -1574,37 +1616,42 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
           segp[a + 1] = segp[a] + (int)((sz + cfg->max_num_seqs - 1) / cfg->max_num_seqs);
         }
       }
-      int *d_segp = nullptr, *d_nt = nullptr;
-      double* d_terms = nullptr;
-      void* scratch = nullptr;  // stream-ordered pool scratch, freed after the kernels
-      if (seg_fs) {
-        const size_t ns = (size_t)std::max(segp[R], 1);
-        const size_t b_terms = ns * bound * sizeof(double), b_nt = (ns * 4 + 255) & ~(size_t)255;
-        const size_t b_segp = ((size_t)(R + 1) * 4 + 255) & ~(size_t)255;
-        if (cudaMallocAsync(&scratch, b_terms + b_nt + b_segp, 0) != cudaSuccess)
-          return fail(RS_ENOMEM, "first-sight scratch");
-        d_terms = (double*)scratch;
-        d_nt = (int*)((char*)scratch + b_terms);
-        d_segp = (int*)((char*)scratch + b_terms + b_nt);
-        if (cudaMemcpyAsync(d_segp, segp.data(), (size_t)(R + 1) * 4, cudaMemcpyHostToDevice, 0) != cudaSuccess)
-          return fail(RS_ECUDA, "first-sight segment upload");
-      }
-      TRY(stage_flush(h));  // the kernels read the rows and write fsprio
-      if (seg_fs) {
-        const int ns = segp[R];
-        const int grid = (int)std::min<long long>((ns + kWarps - 1) / kWarps, 148 * 4);
-        if (ns > 0)
-          first_sight_seg_kernel<<<grid, kThreads>>>((int)R, ns, d_off, d_ol, d_segp, d.tok, m, (int)bound, d_terms,
-                                                     d_nt);
-        first_sight_sum_kernel<<<(unsigned)std::min<long long>((R + 255) / 256, 148 * 4), 256>>>(
-            (int)R, d_segp, (int)bound, d_terms, d_nt, (double*)d.fsprio);
-        cudaFreeAsync(scratch, 0);
+      int* d_segp = nullptr;
+      if (seg_fs) TRY(dalloc(h, &d_segp, R + 1, segp.data()));
+      const int ns = seg_fs ? segp[R] : 0;
+      const int Ri = (int)R;
+      const int* tokp = d.tok;
+      double* fsp = (double*)d.fsprio;
+      auto launch = [=]() -> int {
+        if (seg_fs) {
+          // terms scratch from the stream-ordered pool, freed after the kernels
+          const size_t n_seg = (size_t)std::max(ns, 1);
+          const size_t b_terms = n_seg * bound * sizeof(double);
+          void* scratch = nullptr;
+          if (cudaMallocAsync(&scratch, b_terms + n_seg * 4, 0) != cudaSuccess)
+            return fail(RS_ENOMEM, "first-sight scratch");
+          double* d_terms = (double*)scratch;
+          int* d_nt = (int*)((char*)scratch + b_terms);
+          const int grid = (int)std::min<long long>((ns + kWarps - 1) / kWarps, 148 * 4);
+          if (ns > 0)
+            first_sight_seg_kernel<<<grid, kThreads>>>(Ri, ns, d_off, d_ol, d_segp, tokp, m, (int)bound, d_terms,
+                                                       d_nt);
+          first_sight_sum_kernel<<<(unsigned)std::min<long long>((Ri + 255) / 256, 148 * 4), 256>>>(
+              Ri, d_segp, (int)bound, d_terms, d_nt, fsp);
+          cudaFreeAsync(scratch, 0);
+        } else {
+          const int grid = (int)std::min<long long>((Ri + kWarps - 1) / kWarps, 148 * 8);
+          first_sight_kernel<<<grid, kThreads>>>(Ri, d_off, d_ol, tokp, m, fsp);
+        }
+        const cudaError_t ke = cudaGetLastError();  // stream-ordered before the static-order sort
+        return ke == cudaSuccess ? RS_OK : fail(RS_ECUDA, std::string("first-sight kernels: ") + cudaGetErrorString(ke));
+      };
+      if (h.deferred) {
+        h.pending.push_back(launch);  // after the engine-wide upload (finish_deferred)
       } else {
-        const int grid = (int)std::min<long long>((R + kWarps - 1) / kWarps, 148 * 8);
-        first_sight_kernel<<<grid, kThreads>>>((int)R, d_off, d_ol, d.tok, m, (double*)d.fsprio);
+        TRY(stage_flush(h));  // the kernels read the rows and write fsprio
+        TRY(launch());
       }
-      const cudaError_t ke = cudaGetLastError();  // stream-ordered before the static-order sort below
-      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("first-sight kernels: ") + cudaGetErrorString(ke));
     }
   }
   pc.mark("first-sight kernel");
@@ -1654,7 +1701,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   }
   d.fifo_cap = 1;  // >= capacity + kMaxRun + 2: batched pushes precede evictions
   while (d.fifo_cap < cfg->capacity_blocks + kMaxRun + 2) d.fifo_cap <<= 1;
-  TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
+  TRY(dalloc(h, &d.fifo, d.fifo_cap));  // entries in [head, tail) are written before they are read
   {
     JumpEntry tab[kJumpBits + 32];
     pcg_jump_table(rng, tab);
@@ -1666,7 +1713,14 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   if (log_cap > 0) {
     d.log_cap = 1;
     while (d.log_cap < log_cap) d.log_cap <<= 1;
-    TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
+    TRY(dalloc(h, &d.log, d.log_cap));  // records are written whole before they are read
+  } else {  // no log kept: a one-record scratch ring, so the common-configuration kernel (which always
+            // writes the record) still applies; status.n_log counts, rs_engine_read_log refuses
+    TRY(dalloc(h, &d.log, 1));
+    d.log_cap = 1;
+    h.no_log = true;
+  }
+  if (log_cap > 0) {
     if (cfg->record_order) {  // parity mode snapshots (outside the arena: they can be large)
       const size_t cells = (size_t)d.log_cap * std::max<long long>(R, 1);
       TRY(dalloc(h, &d.snap_prio, cells, nullptr, 0xFF));
@@ -1682,10 +1736,12 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   rc = dalloc(h, &d.ctl, 1, ctl);
   free(ctl);
   if (rc) return rc;
-  rc = stage_flush(h);
-  h.staging = false;
-  std::vector<unsigned char>().swap(h.stage);
-  if (rc) return rc;
+  if (!h.deferred) {
+    rc = stage_flush(h);
+    h.staging = false;
+    std::vector<unsigned char>().swap(h.stage);
+    if (rc) return rc;
+  }
   pc.mark("uploads");
   // the static waiting order on the device: keys from the first-sight
   // priorities (or sp's static ones in the uploaded table), sorted stably in
@@ -1695,10 +1751,15 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
     const RqView dv = rq_carve(d.rq_global, (int)R);
     if (zsort) {
       const double* src = dpu ? d.fsprio : dv.prio;
-      static_keys_kernel<<<(unsigned)std::min<long long>((R + 255) / 256, 148 * 8), 256>>>(src, (int)R, zk0, dv.zl);
-      sort_pairs_one_cta<<<1, kSortThreads>>>(zk0, dv.zl, zk1, zv1, (int)R);
-      const cudaError_t ke = cudaGetLastError();
-      if (ke != cudaSuccess) return fail(RS_ECUDA, std::string("static order sort: ") + cudaGetErrorString(ke));
+      const int Ri = (int)R;
+      auto sort = [=]() -> int {
+        static_keys_kernel<<<(unsigned)std::min<long long>((Ri + 255) / 256, 148 * 8), 256>>>(src, Ri, zk0, dv.zl);
+        sort_pairs_one_cta<<<1, kSortThreads>>>(zk0, dv.zl, zk1, zv1, Ri);
+        const cudaError_t ke = cudaGetLastError();
+        return ke == cudaSuccess ? RS_OK : fail(RS_ECUDA, std::string("static order sort: ") + cudaGetErrorString(ke));
+      };
+      if (h.deferred) h.pending.push_back(sort);
+      else if ((rc = sort())) return rc;
     } else if (R > kSortOneCta && (dpu || cfg->policy == RS_POLICY_SP)) {  // the multi-CTA passes (synchronous)
       DevBuf b;
       unsigned long long* k = nullptr;
@@ -1761,7 +1822,7 @@ static int clone_replica(const HostTrace& src, const rs_config* cfg, const rs_pc
   TRY(dalloc(h, &d.lde, R, nullptr, 0xFF));
   TRY(dalloc(h, &d.gen, N, nullptr, 0));
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
-  TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1), nullptr, 0));
+  TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1)));  // scratch: written before read
   {
     RqView hv = rq_carve(h.rq_host.data(), (int)R);
     int nz = 0;
@@ -1777,8 +1838,8 @@ static int clone_replica(const HostTrace& src, const rs_config* cfg, const rs_pc
         cudaMemcpy((unsigned char*)d.rq_global + zl_at, hv.zl, (size_t)R * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(RS_ECUDA, "replica relQuery table copy failed");
   }
-  TRY(dalloc(h, &d.fifo, d.fifo_cap, nullptr, 0));
-  if (d.log_cap > 0) TRY(dalloc(h, &d.log, d.log_cap, nullptr, 0));
+  TRY(dalloc(h, &d.fifo, d.fifo_cap));  // entries in [head, tail) are written before they are read
+  if (d.log_cap > 0) TRY(dalloc(h, &d.log, d.log_cap));
   Ctl* ctl = (Ctl*)calloc(1, sizeof(Ctl));
   if (!ctl) return fail(RS_ENOMEM, "host alloc");
   ctl->status = RS_RUNNING;
@@ -1799,6 +1860,85 @@ static int upload_traces(rs_engine* e) {
     return fail(RS_ECUDA, "trace table upload failed");
   return RS_OK;
 }
+
+// The deferred small traces (build_trace): their staged arena images go up in
+// one page-locked batch of asynchronous copies, then each trace's creation
+// kernels (first sight, static-order sort) are launched, all stream-ordered on
+// the legacy stream -- no host round trip per trace.
+static int finish_deferred(rs_engine* e, bool with_table) {
+  size_t total = 0;
+  for (auto& h : e->traces)
+    if (h.deferred) total += h.arena_used - h.staged_lo;
+  const size_t table = with_table ? ((sizeof(TraceDev) * e->traces.size() + 255) & ~(size_t)255) : 0;
+  if (with_table) {
+    total += table;
+    if (!e->d_traces && cudaMallocAsync(&e->d_traces, sizeof(TraceDev) * e->traces.size(), 0) != cudaSuccess)
+      return fail(RS_ECUDA, "trace table allocation failed");
+  }
+  if (total) {
+    std::lock_guard<std::mutex> lk(g_pinned.mu);
+    if (g_pinned.done) cudaEventSynchronize(g_pinned.done);  // the previous creation's copies are done
+    if (g_pinned.cap < total) {
+      if (g_pinned.p) cudaFreeHost(g_pinned.p);
+      g_pinned.p = nullptr;
+      g_pinned.cap = 0;
+      const size_t want = total + total / 4 + (1 << 20);
+      if (cudaMallocHost((void**)&g_pinned.p, want) == cudaSuccess) g_pinned.cap = want;
+    }
+    size_t o = 0;
+    if (with_table) {  // the trace table (every pointer is final once the traces are built)
+      for (size_t t = 0; t < e->traces.size(); ++t) {
+        if (g_pinned.p) memcpy(g_pinned.p + t * sizeof(TraceDev), &e->traces[t].dev, sizeof(TraceDev));
+      }
+      const cudaError_t ce =
+          g_pinned.p ? cudaMemcpyAsync(e->d_traces, g_pinned.p, sizeof(TraceDev) * e->traces.size(),
+                                       cudaMemcpyHostToDevice, 0)
+                     : cudaSuccess;
+      if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("trace table upload: ") + cudaGetErrorString(ce));
+      o += table;
+    }
+    for (auto& h : e->traces) {
+      if (!h.deferred) continue;
+      const size_t n = h.arena_used - h.staged_lo;
+      if (!n) continue;
+      cudaError_t ce;
+      if (g_pinned.p) {
+        memcpy(g_pinned.p + o, h.stage.data() + h.staged_lo, n);
+        ce = cudaMemcpyAsync(h.arena + h.staged_lo, g_pinned.p + o, n, cudaMemcpyHostToDevice, 0);
+        o += n;
+      } else {  // no page-locked memory: a staged copy per trace
+        ce = cudaMemcpy(h.arena + h.staged_lo, h.stage.data() + h.staged_lo, n, cudaMemcpyHostToDevice);
+      }
+      if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("deferred upload: ") + cudaGetErrorString(ce));
+      h.staged_lo = h.arena_used;
+    }
+    if (g_pinned.p) {
+      if (!g_pinned.done) cudaEventCreateWithFlags(&g_pinned.done, cudaEventDisableTiming);
+      cudaEventRecord(g_pinned.done, 0);
+    }
+  }
+  if (with_table && !g_pinned.p) {  // no page-locked memory: the synchronous path
+    const int rc = upload_traces(e);
+    if (rc) return rc;
+  }
+  for (auto& h : e->traces) {
+    if (!h.deferred) continue;
+    h.staging = false;
+    std::vector<unsigned char>().swap(h.stage);
+    for (auto& f : h.pending) {
+      const int rc = f();
+      if (rc) return rc;
+    }
+    h.pending.clear();
+    h.deferred = false;
+  }
+  // creation returns without waiting: the first launch (or status read) waits for this
+  if (!e->ready && cudaEventCreateWithFlags(&e->ready, cudaEventDisableTiming) != cudaSuccess)
+    return fail(RS_ECUDA, "creation event");
+  if (cudaEventRecord(e->ready, 0) != cudaSuccess) return fail(RS_ECUDA, "creation event record");
+  return RS_OK;
+}
+
 
 // shard_world == 1: independent traces.  shard_world > 1: every trace is a
 // replica of one trace; replica t is shard t when shard_rank == -1 (all
@@ -1825,6 +1965,21 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
     g_err = keep;
     return code;
   };
+  if (shard_world == 1 && n_traces > 1) {  // independent traces: one arena, sliced (one allocation)
+    std::vector<size_t> needs(n_traces);
+    size_t total = 0;
+    for (int t = 0; t < n_traces; ++t) total += needs[t] = arena_need(traces[t], cfg, log_capacity);
+    void* q = nullptr;
+    if (cudaMallocAsync(&q, total, 0) != cudaSuccess) return bail(fail(RS_ENOMEM, "engine arena"));
+    size_t o = 0;
+    for (int t = 0; t < n_traces; ++t) {
+      HostTrace& h = e->traces[t];
+      h.arena_alloc = t == 0 ? q : nullptr;  // trace 0 owns (frees) the allocation
+      h.arena = (char*)q + o;
+      h.arena_cap = needs[t];
+      o += needs[t];
+    }
+  }
   for (int t = 0; t < n_traces; ++t) {
     const int srank = shard_world == 1 ? 0 : (shard_rank < 0 ? t : shard_rank);
     if (shard_world > 1 && shard_rank < 0 && t > 0)  // another shard of the same pool on this device
@@ -1833,6 +1988,20 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
       rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t], shard_world, srank);
     if (rc) return bail(rc);
   }
+  // shared memory: the control block etc., plus the relQuery table of every
+  // trace whose table fits next to it (the others read theirs from HBM)
+  const size_t base = (sizeof(Shared) + 15) & ~(size_t)15;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  size_t need = base;
+  for (auto& h : e->traces) {
+    const size_t rb = rq_bytes(h.dev.R);
+    h.dev.rq_in_smem = base + rb <= (size_t)max_optin;
+    if (h.dev.rq_in_smem) need = std::max(need, base + rb);
+  }
+  bool all_deferred = shard_world == 1;
+  for (auto& h : e->traces) all_deferred = all_deferred && h.deferred;
+  if ((rc = finish_deferred(e, all_deferred))) return bail(rc);
   if (shard_world > 1) {  // mailboxes (shard.cuh); zeroed: sequence numbers start at 1
     const size_t mb = mailbox_bytes(shard_world);
     const int n_mb = shard_rank < 0 ? shard_world : 1;
@@ -1851,18 +2020,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
     e->connected = shard_rank < 0;
   }
   pc.mark("traces built");
-  // shared memory: the control block etc., plus the relQuery table of every
-  // trace whose table fits next to it (the others read theirs from HBM)
-  const size_t base = (sizeof(Shared) + 15) & ~(size_t)15;
-  int max_optin = 0;
-  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  size_t need = base;
-  for (auto& h : e->traces) {
-    const size_t rb = rq_bytes(h.dev.R);
-    h.dev.rq_in_smem = base + rb <= (size_t)max_optin;
-    if (h.dev.rq_in_smem) need = std::max(need, base + rb);
-  }
-  if ((rc = upload_traces(e))) return bail(rc);
+  if (!all_deferred && (rc = upload_traces(e))) return bail(rc);
   pc.mark("trace table");
   Params& p = e->params;
   p.traces = e->d_traces;
@@ -1980,8 +2138,11 @@ int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
       if (!h.noise_buf) return fail(RS_EINVAL, "noise_sigma > 0 needs rs_engine_set_noise before stepping");
   if (e->shard_world > 1 && !e->connected) return fail(RS_EINVAL, "sharded engine not connected to its peers");
   RS_CUDA(cudaSetDevice(e->device));
-  long long cap = e->params.cfg.log_decisions ? e->traces[0].dev.log_cap : max_iters;
-  if (e->params.cfg.log_decisions && cap > 0 && max_iters > cap) max_iters = cap;
+  // a launch writes at most one ring of records (the host reads them between launches)
+  const bool logs = e->params.cfg.log_decisions && !e->traces[0].no_log;
+  const long long cap = logs ? e->traces[0].dev.log_cap : max_iters;
+  if (logs && cap > 0 && max_iters > cap) max_iters = cap;
+  if (e->ready) RS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, e->ready, 0));  // creation's uploads / kernels
   Params p = e->params;
   p.max_iters = max_iters;
   if (e->common)
@@ -1999,12 +2160,29 @@ int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
 int rs_engine_status(rs_engine* e, void* stream, rs_trace_status* st) {
   if (!e) return fail(RS_EINVAL, "null engine");
   RS_CUDA(cudaSetDevice(e->device));
-  RS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-  const size_t head = offsetof(Ctl, run_row);
-  std::vector<unsigned char> buf(head);
+  // every trace's control-block header into page-locked memory, ordered after the
+  // stream's launches, then one synchronisation
+  const size_t head = (offsetof(Ctl, run_row) + 15) & ~(size_t)15;
+  const size_t total = head * e->traces.size();
+  static std::mutex mu;
+  static unsigned char* buf = nullptr;
+  static size_t cap = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cap < total) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    RS_CUDA(cudaMallocHost((void**)&buf, std::max<size_t>(total, 64 << 10)));
+    cap = std::max<size_t>(total, 64 << 10);
+  }
+  const cudaStream_t strm = (cudaStream_t)stream;
+  if (e->ready) RS_CUDA(cudaStreamWaitEvent(strm, e->ready, 0));
+  for (size_t t = 0; t < e->traces.size(); ++t)
+    RS_CUDA(cudaMemcpyAsync(buf + t * head, e->traces[t].dev.ctl, offsetof(Ctl, run_row), cudaMemcpyDeviceToHost,
+                            strm));
+  RS_CUDA(cudaStreamSynchronize(strm));
   for (size_t t = 0; t < e->traces.size(); ++t) {
-    RS_CUDA(cudaMemcpy(buf.data(), e->traces[t].dev.ctl, head, cudaMemcpyDeviceToHost));
-    const Ctl* c = reinterpret_cast<const Ctl*>(buf.data());
+    const Ctl* c = reinterpret_cast<const Ctl*>(buf + t * head);
     rs_trace_status& s = st[t];
     s.iterations = c->iteration;
     s.clock = c->clock;
@@ -2028,6 +2206,7 @@ int rs_engine_read_log(rs_engine* e, int32_t t, int64_t first, int64_t count, rs
   if (!e || t < 0 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
   const TraceDev& d = e->traces[t].dev;
   if (count <= 0) return RS_OK;
+  if (e->traces[t].no_log) return fail(RS_EINVAL, "engine created without a decision log (log_capacity 0)");
   if (d.log_cap <= 0 || count > d.log_cap) return fail(RS_EINVAL, "log range exceeds the ring buffer");
   RS_CUDA(cudaSetDevice(e->device));
   long long done = 0;
@@ -2182,6 +2361,62 @@ int rs_engine_read_order(rs_engine* e, int32_t t, int64_t first, int64_t count, 
   return RS_OK;
 }
 
+int rs_engine_read_results(rs_engine* e, void* stream, double* fps, double* lpe, double* lde, int32_t* completion_iter) {
+  if (!e) return fail(RS_EINVAL, "null engine");
+  RS_CUDA(cudaSetDevice(e->device));
+  // every trace's device columns into one page-locked buffer, one synchronisation
+  size_t total = 0;
+  for (auto& h : e->traces) total += 24 * (size_t)h.dev.R + 4 * (size_t)h.dev.N;
+  static std::mutex mu;
+  static unsigned char* buf = nullptr;
+  static size_t cap = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cap < total) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    RS_CUDA(cudaMallocHost((void**)&buf, total + total / 4 + 4096));
+    cap = total + total / 4 + 4096;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (e->ready) RS_CUDA(cudaStreamWaitEvent(st, e->ready, 0));
+  size_t o = 0;
+  for (auto& h : e->traces) {
+    const TraceDev& d = h.dev;
+    if (d.R) {
+      RS_CUDA(cudaMemcpyAsync(buf + o, d.fps, 8 * (size_t)d.R, cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaMemcpyAsync(buf + o + 8 * (size_t)d.R, d.lpe, 8 * (size_t)d.R, cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaMemcpyAsync(buf + o + 16 * (size_t)d.R, d.lde, 8 * (size_t)d.R, cudaMemcpyDeviceToHost, st));
+    }
+    if (d.N) RS_CUDA(cudaMemcpyAsync(buf + o + 24 * (size_t)d.R, d.comp, 4 * (size_t)d.N, cudaMemcpyDeviceToHost, st));
+    o += 24 * (size_t)d.R + 4 * (size_t)d.N;
+  }
+  RS_CUDA(cudaStreamSynchronize(st));
+  // ranks -> trace order, traces concatenated
+  o = 0;
+  size_t ro = 0, no = 0;
+  for (auto& h : e->traces) {
+    const int R = h.dev.R, N = h.dev.N;
+    const double* b = (const double*)(buf + o);
+    for (int a = 0; a < R; ++a) {
+      const size_t i = ro + h.order[a];
+      if (fps) fps[i] = b[a];
+      if (lpe) lpe[i] = b[R + a];
+      if (lde) lde[i] = b[2 * R + a];
+    }
+    const int* cp = (const int*)(buf + o + 24 * (size_t)R);
+    if (completion_iter) {
+      if (h.row_src.empty()) memcpy(completion_iter + no, cp, 4 * (size_t)N);
+      else
+        for (int k = 0; k < N; ++k) completion_iter[no + h.row_src[k]] = cp[k];
+    }
+    o += 24 * (size_t)R + 4 * (size_t)N;
+    ro += R;
+    no += N;
+  }
+  return RS_OK;
+}
+
 int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* fps, double* lpe, double* lde) {
   if (!e || t < 0 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
   const HostTrace& h = e->traces[t];
@@ -2265,6 +2500,10 @@ void rs_engine_destroy(rs_engine* e) {
   if (e->done) {  // the last launch may still run on a non-blocking stream
     cudaEventSynchronize(e->done);
     cudaEventDestroy(e->done);
+  }
+  if (e->ready) {
+    cudaEventSynchronize(e->ready);
+    cudaEventDestroy(e->ready);
   }
   if (e->mbox) cudaFree(e->mbox);
   if (e->d_peers) cudaFree(e->d_peers);
