@@ -144,10 +144,15 @@ def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # tests only: every rank on one device (the multi-rank path on a one-GPU box; NCCL refuses
+    # two ranks per GPU, so the plumbing goes over gloo)
+    shared = os.environ.get("RS_BENCH_DEVICE")
+    if shared is not None:
+        local = int(shared)
     if ws > 1:
         import torch.distributed as dist
 
-        backend = "nccl" if args.impl == "ours" else "gloo"
+        backend = "nccl" if args.impl == "ours" and shared is None else "gloo"
         if backend == "nccl":
             import torch
 

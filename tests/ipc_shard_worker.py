@@ -1,6 +1,8 @@
 """Helper for tests/test_gpu_sharded.py::test_two_process_shards_over_ipc: one
 shard of a sharded pool per process (mailboxes exchanged as CUDA IPC handles
-over a gloo group), both on GPU 0.  Not collected by pytest (no test_ prefix)."""
+over a gloo group), all on GPU 0 -- or, with RS_IPC_DEVICE_PER_RANK=1, rank r on
+GPU r (tests/test_gpu_multigpu.py: the NVLink peer-memory path).  Not collected
+by pytest (no test_ prefix)."""
 
 import os
 import sys
@@ -19,9 +21,11 @@ def main(rank: int, world: int, port: int, out_path: str):
     from paper_2601_11546_b200 import EngineConfig, TraceConfig, generate_trace, sharded, world_preset
     from paper_2601_11546_b200.engine import Engine, SimulationAborted
 
-    trace = generate_trace(TraceConfig(num_relqueries=40, size_range=(1, 60), rate=4.0, seed=9))
+    n_rq = int(os.environ.get("RS_IPC_RELQUERIES", "40"))
+    trace = generate_trace(TraceConfig(num_relqueries=n_rq, size_range=(1, 60), rate=4.0, seed=9))
     cfg = EngineConfig(iteration_limit=int(os.environ.get("RS_IPC_ITERS", "40")))
-    eng = Engine(trace, "relserve", world_preset("opt-13b-like"), cfg, device=0, shards=world, shard_rank=rank)
+    device = rank if os.environ.get("RS_IPC_DEVICE_PER_RANK") == "1" else 0
+    eng = Engine(trace, "relserve", world_preset("opt-13b-like"), cfg, device=device, shards=world, shard_rank=rank)
     sharded.connect(eng)
     try:
         res = eng.run()
