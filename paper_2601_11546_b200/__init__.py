@@ -26,15 +26,20 @@ from .engine import (
     run,
 )
 from .priority import (
+    CacheMissRatio,
+    DynamicPriorityUpdater,
     InfeasibleRequestError,
     PriorityRecord,
     RemainderItem,
     SchedulerConstraints,
+    apply_starvation_override,
     pem,
     pem_batch,
     remainder_items,
+    sample_cache_miss_ratio,
     static_relquery_prio,
     static_req_prio,
+    utok_approx,
 )
 from .report import SummaryTable, decompose, summarize
 from .workload import (
@@ -52,11 +57,11 @@ from .workload import (
 )
 
 __all__ = [
-    "ArrivalTrace", "DecisionLogEntry", "decompose", "Engine", "EngineConfig", "InfeasibleRequestError",
+    "apply_starvation_override", "ArrivalTrace", "CacheMissRatio", "DecisionLogEntry", "DynamicPriorityUpdater", "decompose", "Engine", "EngineConfig", "InfeasibleRequestError",
     "LinearCostModel", "OUTPUT_LIMITS", "POLICIES", "PriorityRecord", "QueryType", "RelQuery",
     "RemainderItem", "Request", "RunResult", "SchedulerConstraints", "SimulationAborted",
     "TimestampLedger", "TraceColumns", "TraceConfig", "WORLD_PRESETS", "generate_heavy_tail_trace",
     "generate_trace", "load_model", "load_trace", "pem", "pem_batch", "predict_decode", "predict_prefill",
-    "remainder_items", "run", "save_model", "save_trace", "static_relquery_prio", "static_req_prio",
-    "summarize", "SummaryTable", "world_preset",
+    "remainder_items", "run", "sample_cache_miss_ratio", "save_model", "save_trace", "static_relquery_prio", "static_req_prio",
+    "summarize", "SummaryTable", "utok_approx", "world_preset",
 ]
