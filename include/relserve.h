@@ -234,6 +234,13 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
                             int64_t* completion_iter, double* priority);
 
 /*
+ * The running list between steps (Engine.running, engine.py:205, 326-329,
+ * 358-359): the trace-order row index of every running request in execution
+ * order.  Writes min(n_running, cap) rows and the full count to *n_running.
+ */
+int rs_engine_read_running(rs_engine* e, int32_t t, int32_t* rows, int32_t cap, int32_t* n_running);
+
+/*
  * Every trace's results at once (multi-trace engines, e.g. a sweep of
  * independent traces): the ledgers' first_prefill_start / last_prefill_end /
  * last_decode_end (NaN = None) of all relQueries and the completion iteration

@@ -51,6 +51,8 @@ def lib():
     L.rs_engine_read_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
     L.rs_waiting_argmin.restype = C.c_int
     L.rs_waiting_argmin.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
+    L.rs_engine_read_running.restype = C.c_int
+    L.rs_engine_read_running.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
     L.rs_engine_read_completion.restype = C.c_int
     L.rs_engine_read_completion.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
     L.rs_engine_destroy.restype = None
@@ -112,6 +114,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_build_info", "rs_engine_create", "rs_engine_step", "rs_engine_status",
     "rs_engine_read_log", "rs_engine_read_ledgers", "rs_engine_read_requests", "rs_engine_read_completion",
+    "rs_engine_read_running",
     "rs_engine_destroy", "rs_engine_device_bytes", "rs_pem_batch", "rs_choice_sequence", "rs_device_clock_khz",
     "rs_engine_create_sharded", "rs_engine_mailbox", "rs_engine_connect", "rs_ipc_get_handle",
     "rs_ipc_open_handle", "rs_ipc_close", "rs_engine_set_noise", "rs_arrange", "rs_waiting_argmin",
@@ -258,6 +261,16 @@ class NativeEngine:
         _check(lib().rs_engine_read_requests(self.h, t, gen.ctypes.data, pre.ctypes.data,
                                              comp.ctypes.data, prio.ctypes.data))
         return gen, pre, comp, prio
+
+    def read_running(self, t: int) -> np.ndarray:
+        """Trace-order rows of the running requests, in execution order."""
+        n = C.c_int32(0)
+        rows = np.zeros(1024, np.int32)
+        _check(lib().rs_engine_read_running(self.h, t, rows.ctypes.data, len(rows), C.byref(n)))
+        if n.value > len(rows):
+            rows = np.zeros(n.value, np.int32)
+            _check(lib().rs_engine_read_running(self.h, t, rows.ctypes.data, len(rows), C.byref(n)))
+        return rows[: n.value].copy()
 
     def read_completion(self, t: int, N: int) -> np.ndarray:
         """int32 completion iterations, trace order, in page-locked memory from torch's caching

@@ -2478,6 +2478,25 @@ int rs_engine_read_requests(rs_engine* e, int32_t t, int32_t* generated, uint8_t
   return RS_OK;
 }
 
+int rs_engine_read_running(rs_engine* e, int32_t t, int32_t* rows, int32_t cap, int32_t* n_running) {
+  if (!e || t < 0 || t >= (int)e->traces.size() || !n_running || cap < 0 || (cap > 0 && !rows))
+    return fail(RS_EINVAL, "bad arguments");
+  const HostTrace& h = e->traces[t];
+  RS_CUDA(cudaSetDevice(e->device));
+  if (e->ready) RS_CUDA(cudaEventSynchronize(e->ready));
+  int n = 0;
+  RS_CUDA(cudaMemcpy(&n, (const char*)h.dev.ctl + offsetof(Ctl, n_run), sizeof(int), cudaMemcpyDeviceToHost));
+  *n_running = n;
+  const int k = n < cap ? n : cap;
+  if (k > 0) {
+    std::vector<int> rr(k);
+    RS_CUDA(cudaMemcpy(rr.data(), (const char*)h.dev.ctl + offsetof(Ctl, run_row), sizeof(int) * k,
+                       cudaMemcpyDeviceToHost));
+    for (int i = 0; i < k; ++i) rows[i] = (int32_t)(h.row_src.empty() ? rr[i] : h.row_src[rr[i]]);
+  }
+  return RS_OK;
+}
+
 int rs_engine_read_completion(rs_engine* e, int32_t t, int32_t* completion_iter) {
   if (!e || t < 0 || t >= (int)e->traces.size()) return fail(RS_EINVAL, "bad trace index");
   const HostTrace& h = e->traces[t];

@@ -100,6 +100,26 @@ class RunResult:
             return 0.0
         return (self.dpu_wall_s + self.aba_wall_s) / self.sim_duration
 
+    def to_relsim(self, engine_module=None):
+        """The same result as a genuine ``relsim.engine.RunResult`` (engine.py:77-138), for
+        callers that type-check or pickle relsim objects.  ``engine_module`` defaults to
+        ``relsim.engine`` (imported on demand; this package never needs relsim itself)."""
+        if engine_module is None:
+            import importlib
+
+            engine_module = importlib.import_module("relsim.engine")
+        L, D = engine_module.TimestampLedger, engine_module.DecisionLogEntry
+        return engine_module.RunResult(
+            policy=self.policy, rate=self.rate, seed=self.seed,
+            ledgers={k: L(v.arrival, v.first_prefill_start, v.last_prefill_end, v.last_decode_end)
+                     for k, v in self.ledgers.items()},
+            relquery_sizes=dict(self.relquery_sizes),
+            decision_log=[D(e.iteration, e.clock, e.case, e.m_plus, e.m_minus, e.delta_plus, e.delta_minus,
+                            e.delta_total, e.action) for e in self.decision_log],
+            iterations=self.iterations, sim_duration=self.sim_duration, dpu_wall_s=self.dpu_wall_s,
+            aba_wall_s=self.aba_wall_s, cache_hit_tokens=self.cache_hit_tokens,
+            cache_miss_tokens=self.cache_miss_tokens)
+
     def write_relquery_csv(self, path) -> None:
         """Per-relQuery latency breakdown in rel_id order, floats as repr (engine.py:104-125)."""
         import csv
@@ -275,6 +295,25 @@ def raise_for(code: int, msg: str):
     if code in (_abi.RS_OK, _abi.RS_RUNNING):
         return
     raise _ERRORS.get(code, RuntimeError)(msg)
+
+
+class WaitingEntry:
+    """relsim's _WaitingEntry (engine.py:160-176): a relQuery's not-yet-prefilled requests."""
+
+    __slots__ = ("relquery", "pending", "arrival_index", "_priority")
+
+    def __init__(self, relquery, arrival_index: int):
+        self.relquery = relquery
+        self.pending = list(relquery.requests)
+        self.arrival_index = arrival_index
+        self._priority = 0.0
+
+    @property
+    def priority(self) -> float:
+        return self._priority if self.pending else 0.0
+
+    def sort_key(self):
+        return (self.priority, self.relquery.arrival, self.relquery.rel_id)
 
 
 class Engine:
@@ -498,24 +537,47 @@ class Engine:
         khz = _native.device_clock_khz(self.device)
         return sum(int(st.phase_cycles[k]) for k in phases) / (khz * 1e3) if khz else 0.0
 
+    def _row_objects(self):
+        """Trace-order row k -> its Request object (reference objects, built on first use)."""
+        if getattr(self, "_rows", None) is None:
+            self._rows = [r for q in self.trace.entries for r in q.requests]
+        return self._rows
+
+    @property
+    def running_rows(self) -> np.ndarray:
+        """Trace-order request indices of the running list, in execution order (no objects)."""
+        return self._native.read_running(0)
+
     @property
     def running(self) -> list:
-        """Requests prefilled and not done (empty once the run finished)."""
-        if self.result is None:
-            return []
-        gen, pre, _, _ = self.requests_state
-        c = self.trace.columns()
-        idx = np.nonzero((pre != 0) & (gen < c.out))[0]
-        return idx.tolist()
+        """relsim's ``Engine.running`` (engine.py:205): the prefilled, unfinished requests in
+        execution order, as the trace's Request objects, read from the device between steps."""
+        rows = self._row_objects()
+        return [rows[k] for k in self.running_rows.tolist()]
 
     @property
     def waiting(self) -> list:
-        if self.result is None:
-            return []
-        _, pre, _, _ = self.requests_state
+        """relsim's ``Engine.waiting`` (engine.py:160-176, 205, 277-281) between steps: one
+        WaitingEntry per admitted relQuery with unprefilled requests, ordered by
+        (priority, arrival, rel_id) -- the order of the last iteration's sort, whose head's
+        prefilled rows have left ``pending``."""
         c = self.trace.columns()
-        rq = np.repeat(np.arange(c.num_relqueries), np.diff(c.row_off))
-        return sorted(set(rq[pre == 0].tolist()))
+        adm = np.lexsort((c.rel_id, c.arrival))  # admission order (engine.py:211-213)
+        n_adm = int(self._status.admitted) if self._status is not None else 0
+        _, pre, _, prio = self._native.read_requests(0, c.num_requests)
+        entries = self.trace.entries
+        out = []
+        for ai, i in enumerate(adm[:n_adm].tolist()):
+            lo, hi = int(c.row_off[i]), int(c.row_off[i + 1])
+            n_pre = int(pre[lo:hi].sum())
+            if n_pre < hi - lo:
+                q = entries[i]
+                e = WaitingEntry(q, ai)
+                e.pending = q.requests[n_pre:]
+                e._priority = float(prio[lo]) if hi > lo else 0.0
+                out.append(e)
+        out.sort(key=WaitingEntry.sort_key)
+        return out
 
     def close(self):
         if getattr(self, "_native", None) is not None:

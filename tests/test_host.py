@@ -181,3 +181,34 @@ def test_fullscale_fingerprint_canonical():
     for name in ("config2", "config3"):
         assert all(f"sha256_{k}" in g["configs"][name] for k in FIELDS)
         assert g["configs"][name]["records"] == g["configs"][name]["iterations"] > 100_000
+
+
+def test_run_result_to_relsim_types():
+    """RunResult.to_relsim() builds the reference's own RunResult (engine.py:77-138)
+    field for field; relsim itself is imported when present (build container)."""
+    import math
+    import sys
+    from pathlib import Path
+
+    from paper_2601_11546_b200 import engine as E
+
+    res = E.RunResult("relserve", 1.0, 0, {7: E.TimestampLedger(0.5, 0.6, 0.7, 0.9)}, {7: 3},
+                      [E.DecisionLogEntry(0, 0.0, "forced", None, None, None, None, None, "idle"),
+                       E.DecisionLogEntry(1, 0.5, "transitional", 0.1, 0.2, 0.3, -0.4, -0.1, "prefill")],
+                      2, 0.9, 0.0, 0.0, 5, 7)
+    mods = [E]
+    if Path("/root/reference/pkg/src").exists():
+        sys.path.insert(0, "/root/reference/pkg/src")
+        try:
+            import relsim.engine as RE
+
+            mods.append(RE)
+        finally:
+            sys.path.pop(0)
+    for m in mods:
+        r = res.to_relsim(m)
+        assert type(r) is m.RunResult
+        assert r.ledgers[7] == m.TimestampLedger(0.5, 0.6, 0.7, 0.9)
+        assert [type(e) for e in r.decision_log] == [m.DecisionLogEntry] * 2
+        assert r.decision_log[1].delta_total == -0.1 and r.decision_log[0].m_plus is None
+        assert math.isclose(r.cache_hit_ratio, 5 / 12)
