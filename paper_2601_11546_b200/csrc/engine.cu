@@ -31,6 +31,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -1094,14 +1095,37 @@ struct PhaseClock {
     if (_e != cudaSuccess) return fail(RS_ECUDA, std::string(#call ": ") + cudaGetErrorString(_e)); \
   } while (0)
 
+// A host column shared (not copied) between the replicas of a sharded pool;
+// copy-on-write for the rare replica that changes one.
+template <class T>
+struct SharedVec {
+  std::shared_ptr<std::vector<T>> p = std::make_shared<std::vector<T>>();
+  std::vector<T>& w() {
+    if (p.use_count() > 1) p = std::make_shared<std::vector<T>>(*p);
+    return *p;
+  }
+  const T& operator[](size_t i) const { return (*p)[i]; }
+  T& operator[](size_t i) { return w()[i]; }
+  size_t size() const { return p->size(); }
+  bool empty() const { return p->empty(); }
+  const T* cdata() const { return p->data(); }
+  T* data() { return w().data(); }
+  typename std::vector<T>::iterator begin() { return w().begin(); }
+  typename std::vector<T>::iterator end() { return w().end(); }
+  void resize(size_t n) { w().resize(n); }
+  void assign(size_t n, const T& v) { w().assign(n, v); }
+  template <class It>
+  void assign(It a, It b) { w().assign(a, b); }
+};
+
 struct HostTrace {
   TraceDev dev{};
   rs_cost_model pol{};
-  std::vector<unsigned char> rq_host;  // relQuery table staging (rq_carve layout)
-  std::vector<int> off;                // rank-ordered row offsets
-  std::vector<int> rank_of;     // trace index -> rank
-  std::vector<int> order;       // rank -> trace index
-  std::vector<long long> row_src;  // rank-ordered row -> trace-order row (empty: identity)
+  SharedVec<unsigned char> rq_host;  // relQuery table staging (rq_carve layout)
+  SharedVec<int> off;                // rank-ordered row offsets
+  SharedVec<int> rank_of;     // trace index -> rank
+  SharedVec<int> order;       // rank -> trace index
+  SharedVec<long long> row_src;  // rank-ordered row -> trace-order row (empty: identity)
   std::vector<void*> allocs;
   long long bytes = 0;
   long long log_read = 0;
@@ -1116,7 +1140,7 @@ struct HostTrace {
   bool staging = false;
   std::vector<unsigned char> stage;
   size_t staged_lo = 0;  // arena bytes [staged_lo, arena_used) not uploaded yet
-  std::vector<int> zorder;      // every relQuery in the static waiting order
+  SharedVec<int> zorder;      // every relQuery in the static waiting order
   bool no_log = false;          // created with log_capacity 0 (the device writes a scratch record)
   // small traces: the staged arena image and the creation kernels wait for one
   // engine-wide upload (finish_deferred)
@@ -1824,18 +1848,22 @@ static int clone_replica(const HostTrace& src, const rs_config* cfg, const rs_pc
   TRY(dalloc(h, &d.comp, N, nullptr, 0xFF));
   TRY(dalloc(h, &d.term_spill, (size_t)kMaxJobs * (kSmallMns + 1)));  // scratch: written before read
   {
-    RqView hv = rq_carve(h.rq_host.data(), (int)R);
-    int nz = 0;
+    // the host columns are shard 0's (shared, not copied); only this shard's static order differs
+    const int* zo = h.zorder.cdata();
+    std::vector<int> zl;
+    zl.reserve((size_t)(R / shard_world + 1));
     for (long long i = 0; i < R; ++i)
-      if (h.zorder[i] % shard_world == shard_rank) hv.zl[nz++] = h.zorder[i];
-    d.nzl = nz;
+      if (zo[i] % shard_world == shard_rank) zl.push_back(zo[i]);
+    d.nzl = (int)zl.size();
     d.shard_world = shard_world;
     d.shard_rank = shard_rank;
     // the table is shard 0's (device to device) but for this shard's static order
     TRY(dalloc(h, (unsigned char**)&d.rq_global, h.rq_host.size()));
-    const size_t zl_at = (size_t)((const unsigned char*)hv.zl - h.rq_host.data());
+    const unsigned char* base = h.rq_host.cdata();
+    const size_t zl_at = (size_t)((const unsigned char*)rq_carve(const_cast<unsigned char*>(base), (int)R).zl - base);
     if (cudaMemcpyAsync(d.rq_global, src.dev.rq_global, h.rq_host.size(), cudaMemcpyDeviceToDevice, 0) != cudaSuccess ||
-        cudaMemcpy((unsigned char*)d.rq_global + zl_at, hv.zl, (size_t)R * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+        (!zl.empty() && cudaMemcpy((unsigned char*)d.rq_global + zl_at, zl.data(), zl.size() * sizeof(int),
+                                   cudaMemcpyHostToDevice) != cudaSuccess))
       return fail(RS_ECUDA, "replica relQuery table copy failed");
   }
   TRY(dalloc(h, &d.fifo, d.fifo_cap));  // entries in [head, tail) are written before they are read
@@ -2428,7 +2456,7 @@ int rs_engine_read_ledgers(rs_engine* e, int32_t t, double* arrival, double* fps
     RS_CUDA(cudaMemcpy(c.data(), h.dev.lpe, R * 8, cudaMemcpyDeviceToHost));
     RS_CUDA(cudaMemcpy(d.data(), h.dev.lde, R * 8, cudaMemcpyDeviceToHost));
   }
-  const RqView hv = rq_carve(const_cast<unsigned char*>(h.rq_host.data()), R);
+  const RqView hv = rq_carve(const_cast<unsigned char*>(h.rq_host.cdata()), R);
   for (int r = 0; r < R; ++r) {
     const int i = h.order[r];
     if (arrival) arrival[i] = hv.arrival[r];
