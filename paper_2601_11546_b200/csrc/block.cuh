@@ -300,6 +300,13 @@ __device__ __forceinline__ void handoff_arrive() {  // group D
 __device__ __forceinline__ void handoff_wait() {  // group M
   asm volatile("bar.sync %0, %1;" ::"n"(kBarHandoff), "n"(kThreads) : "memory");
 }
+constexpr int kBarExecDone = 5;  // group M has applied the iteration's action (group D may commit its update)
+__device__ __forceinline__ void exec_done_arrive() {  // group M
+  asm volatile("bar.arrive %0, %1;" ::"n"(kBarExecDone), "n"(kThreads) : "memory");
+}
+__device__ __forceinline__ void exec_done_wait() {  // group D
+  asm volatile("bar.sync %0, %1;" ::"n"(kBarExecDone), "n"(kThreads) : "memory");
+}
 
 // block_scan32 over the G::kN threads of a group (thread index within the group
 // = threadIdx.x - base; the group's warps are consecutive)

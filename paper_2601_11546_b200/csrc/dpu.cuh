@@ -498,9 +498,14 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   const int n_act = c.n_act;
   const bool join = pf && rq.q[h] == 0;  // h's first prefill: it joins the list
   const int n_est = n_act + (join ? 1 : 0);
-  if (!allowed || n_est > kSmallEst || n_est == 0) {  // group-uniform
+#ifdef RS_NO_SPEC  // experiment: the pipelined update disabled (every update runs in place)
+  const bool no_spec = true;
+#else
+  const bool no_spec = false;
+#endif
+  if (no_spec || !allowed || n_est > kSmallEst || n_est == 0) {  // group-uniform
     if (threadIdx.x == kMWarps * 32) {
-      S.spec_valid = n_est == 0 && allowed;  // nothing to re-estimate: trivially done
+      S.spec_valid = !no_spec && n_est == 0 && allowed;  // nothing to re-estimate: trivially done
       S.spec_n = 0;
       S.spec_rng = c.rng;
       S.spec_alg = 0;
@@ -835,7 +840,8 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   dphase_mark(c, 21);
 }
 
-// After the join (warp 0): the speculative update becomes this (next)
+// After the advance (group D's first warp, behind kBarExecDone; group M is
+// already in the next admission): the speculative update becomes this (next)
 // iteration's if every chain length it assumed is the advance's; retiring
 // relQueries (no unprefilled and no running row left) are not written.  The
 // entries kept must be exactly the advance's act list.
@@ -843,7 +849,7 @@ __device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const int lane = threadIdx.x & 31;
-  bool ok = S.spec_valid && c.status == RS_RUNNING;
+  bool ok = S.spec_valid && S.go_exec;  // (c.status may change concurrently: the next admission)
   const int n = S.spec_n;
   bool keep = false, bad = false;
   int a = 0;

@@ -727,16 +727,21 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     // pipelined: group M executes this iteration while group D computes the
     // next iteration's priority update of the partially prefilled relQueries
     // (dpu_spec) from the state this advance leaves; both join at the barrier
+    // The groups do not join here: group M signals the advance done (barrier
+    // kBarExecDone, arrive only) and goes on to the next iteration's admission;
+    // group D, once its update is computed, waits for that signal, commits the
+    // update against the advance's result, and both meet at the admission
+    // barrier -- so the update may run over into the admission.
     const bool allowed = !last && c.iteration + 1 < cfg.iteration_limit;
     if (opaque_warp() < kMWarps) {
       const bool go = execute<kC, GM, true>(P, T, S, action);  // group-uniform
       if (tid == 0) S.go_exec = go;
-    } else {
-      dpu_spec(P, T, S, action, S.head, S.taken, allowed);
+      exec_done_arrive();
+      return go;
     }
-    __syncthreads();
-    phase_mark(c, 1);  // the wait for group D beyond the advance (the update's share of the critical path)
-    if (opaque_warp() == 0) spec_commit(S, T);
+    dpu_spec(P, T, S, action, S.head, S.taken, allowed);
+    exec_done_wait();
+    if (opaque_warp() == kMWarps) spec_commit(S, T);
     return S.go_exec;
   } else {
     return execute<kC, GAll, false>(P, T, S, action);
