@@ -933,59 +933,77 @@ __global__ void __launch_bounds__(kThreads) first_sight_kernel(int R, const int*
 // segment's terms in the reference's order (its prefill sub-batches, then the
 // decode term: pem(), priority.py:187-217, every row unprefilled with utok =
 // tok and remaining = output_limit); first_sight_sum_kernel then adds each
-// relQuery's terms in order.  seg_pref[a] = the first segment of relQuery a.
+// relQuery's terms in order.  seg[sg] = (first row, rows, output limit) of
+// segment sg (host-built).  Each warp walks its segments with the next
+// segment's tok already in flight (coalesced: lane l holds rows l, l+32, ...)
+// and its descriptor two ahead, so HBM latency hides behind the sub-batch
+// chain; the rows are transposed through shared memory (skewed against bank
+// conflicts) so that each lane scans 8 consecutive rows.
 // Terms per segment are bounded by 2*sum(tok)/mnbt + 3 (consecutive next-fit
 // sub-batches exceed mnbt together); the host sizes `bound` from max(tok).
-__global__ void __launch_bounds__(kThreads) first_sight_seg_kernel(int R, int n_seg, const int* off, const int* ol,
-                                                                   const int* seg_pref, const int* tok, PemModel m,
-                                                                   int bound, double* terms, int* nterm) {
-  __shared__ int U[kWarps][kSmallMns];
+__device__ __forceinline__ int fs_skew(int x) { return x + (x >> 5); }
+
+__global__ void __launch_bounds__(kThreads) first_sight_seg_kernel(int n_seg, const int4* seg, const int* tok,
+                                                                   PemModel m, int bound, double* terms, int* nterm) {
+  __shared__ int U[kWarps][kSmallMns + kSmallMns / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int mns = (int)m.mns;
   int* Uw = U[warp];
-  for (int sg = blockIdx.x * kWarps + warp; sg < n_seg; sg += gridDim.x * kWarps) {
-    int lo = 0, hi = R;  // the relQuery: the last a with seg_pref[a] <= sg
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (seg_pref[mid] <= sg) lo = mid;
-      else hi = mid;
-    }
-    const int a = lo, k = sg - seg_pref[a];
-    const int r0 = off[a] + k * mns, r1 = min(off[a + 1], r0 + mns), nloc = r1 - r0;
+  const int stride = gridDim.x * kWarps;
+  int sg = blockIdx.x * kWarps + warp;
+  int4 d_cur = sg < n_seg ? seg[sg] : make_int4(0, 0, 0, 0);
+  int4 d_nxt = sg + stride < n_seg ? seg[sg + stride] : make_int4(0, 0, 0, 0);
+  int nv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) nv[i] = i * 32 + lane < d_cur.y ? tok[d_cur.x + i * 32 + lane] : 0;
+  for (; sg < n_seg; sg += stride) {
+    const int4 d = d_cur;
+    int cv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cv[i] = nv[i];
+    // next segment's rows in flight, the one after's descriptor too
+    d_cur = d_nxt;
+    d_nxt = sg + 2 * stride < n_seg ? seg[sg + 2 * stride] : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) nv[i] = i * 32 + lane < d_cur.y ? tok[d_cur.x + i * 32 + lane] : 0;
+    const int nloc = d.y;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Uw[fs_skew(i * 32 + lane)] = cv[i];
+    __syncwarp();
     const int per = (nloc + 31) >> 5, x0 = lane * per;  // per <= 8
     int uv[8], ls = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      uv[i] = (i < per && x0 + i < nloc) ? tok[r0 + x0 + i] : 0;
+      uv[i] = (i < per && x0 + i < nloc) ? Uw[fs_skew(x0 + i)] : 0;
       ls += uv[i];
     }
     int run = warp_incl_scan(ls) - ls;
+    __syncwarp();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       run += uv[i];
-      if (i < per && x0 + i < nloc) Uw[x0 + i] = run;
+      if (i < per && x0 + i < nloc) Uw[fs_skew(x0 + i)] = run;
     }
     __syncwarp();
     double* tj = terms + (size_t)sg * bound;
     int nt = 0, bb = 0;
     while (bb < nloc) {  // the prefill sub-batch chain (see dpu_small)
-      const int before = bb ? Uw[bb - 1] : 0;
-      const int ub = Uw[bb];
+      const int before = bb ? Uw[fs_skew(bb - 1)] : 0;
+      const int ub = Uw[fs_skew(bb)];
       const int thr = ub - before > m.mnbt ? ub : before + (int)m.mnbt;
       int nb = nloc;
       for (int b2 = bb + 1; b2 < nloc; b2 += 32) {
-        const unsigned mx = __ballot_sync(kFull, b2 + lane < nloc && Uw[b2 + lane] > thr);
+        const unsigned mx = __ballot_sync(kFull, b2 + lane < nloc && Uw[fs_skew(b2 + lane)] > thr);
         if (mx) {
           nb = b2 + __ffs(mx) - 1;
           break;
         }
       }
-      if (lane == 0) tj[nt] = lin(m.ap, (double)(Uw[nb - 1] - before), m.bp);
+      if (lane == 0) tj[nt] = lin(m.ap, (double)(Uw[fs_skew(nb - 1)] - before), m.bp);
       ++nt;
       bb = nb;
     }
     if (lane == 0) {
-      const long long o = ol[a];
+      const long long o = d.z;
       tj[nt] = __dadd_rn(__dmul_rn(m.ad, (double)((long long)nloc * o)), __dmul_rn(m.bd, (double)o));
       nterm[sg] = nt + 1;
     }
@@ -1638,15 +1656,20 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       const long long bound = 2 * cfg->max_num_seqs * max_tok_all / cfg->max_num_batched_tokens + 3;
       const bool seg_fs = d.seg_ok && cfg->max_num_seqs <= kSmallMns && bound <= 64;
       std::vector<int> segp;
+      std::vector<int4> segd;  // per segment: first row, rows, output limit
       if (seg_fs) {
         segp.assign(R + 1, 0);
+        const int mns = (int)cfg->max_num_seqs;
         for (long long a = 0; a < R; ++a) {
-          const long long sz = off[a + 1] - off[a];
-          segp[a + 1] = segp[a] + (int)((sz + cfg->max_num_seqs - 1) / cfg->max_num_seqs);
+          const int sz = off[a + 1] - off[a];
+          segp[a + 1] = segp[a] + (sz + mns - 1) / mns;
+          for (int r = 0; r < sz; r += mns) segd.push_back(make_int4(off[a] + r, std::min(mns, sz - r), ol[a], 0));
         }
       }
       int* d_segp = nullptr;
+      int4* d_segd = nullptr;
       if (seg_fs) TRY(dalloc(h, &d_segp, R + 1, segp.data()));
+      if (seg_fs && !segd.empty()) TRY(dalloc(h, &d_segd, segd.size(), segd.data()));
       const int ns = seg_fs ? segp[R] : 0;
       const int Ri = (int)R;
       const int* tokp = d.tok;
@@ -1663,8 +1686,7 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
           int* d_nt = (int*)((char*)scratch + b_terms);
           const int grid = (int)std::min<long long>((ns + kWarps - 1) / kWarps, 148 * 4);
           if (ns > 0)
-            first_sight_seg_kernel<<<grid, kThreads>>>(Ri, ns, d_off, d_ol, d_segp, tokp, m, (int)bound, d_terms,
-                                                       d_nt);
+            first_sight_seg_kernel<<<grid, kThreads>>>(ns, d_segd, tokp, m, (int)bound, d_terms, d_nt);
           first_sight_sum_kernel<<<(unsigned)std::min<long long>((Ri + 255) / 256, 148 * 4), 256>>>(
               Ri, d_segp, (int)bound, d_terms, d_nt, fsp);
           cudaFreeAsync(scratch, 0);
