@@ -63,10 +63,14 @@ namespace rsd {
 // running relQuery in rel_id order (engine.py:406-408); internal = the first
 // running row attaining m+ belongs to the prefill candidate's relQuery.
 // Outputs follow rs_iter_record: NaN where the reference logs None.
-template <class OL>
+// Proj supplies the projection's per-relQuery terms: term(i, adn, ol_p) =
+// (alpha_d * n_p) * min(OL_i, OL_p) of the i-th distinct running relQuery in
+// rel_id order, and max_ol(n) = max OL over them (the engine precomputes both in
+// parallel; the unit entry point computes them here).
+template <class Proj>
 __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_first, int force, bool has_p,
                                         bool has_d, bool internal, double m_plus, double m_minus, long long utok_sum,
-                                        int n_p, long long ol_p, int n_dist, const OL& ol, long long W, int& action,
+                                        int n_p, long long ol_p, int n_dist, const Proj& pj, long long W, int& action,
                                         int& kase, double& mp, double& mmn, double& dp, double& dm, double& dt) {
   dp = dm = dt = __longlong_as_double(0x7FF8000000000000LL);
   mp = m_plus;
@@ -87,14 +91,16 @@ __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_fir
   if (has_p && has_d && !internal && m_plus <= m_minus) {
     const double l_prefill = __dadd_rn(__dmul_rn(m.alpha_p, (double)utok_sum), m.beta_p);
     ddp = __dmul_rn(l_prefill, (double)n_dist);
-    long long max_ol = 0;
     const double adn = __dmul_rn(m.alpha_d, (double)n_p);
-#pragma unroll 1
-    for (int i = 0; i < n_dist; ++i) {
-      const long long o = ol(i);
-      ddp = __dadd_rn(ddp, __dmul_rn(adn, (double)(o < ol_p ? o : ol_p)));
-      max_ol = o > max_ol ? o : max_ol;
+    int i = 0;
+    for (; i + 4 <= n_dist; i += 4) {  // the adds stay in order; the terms are independent
+      const double t0 = pj.term(i, adn, ol_p), t1 = pj.term(i + 1, adn, ol_p), t2 = pj.term(i + 2, adn, ol_p),
+                   t3 = pj.term(i + 3, adn, ol_p);
+      ddp = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(ddp, t0), t1), t2), t3);
     }
+#pragma unroll 1
+    for (; i < n_dist; ++i) ddp = __dadd_rn(ddp, pj.term(i, adn, ol_p));
+    const long long max_ol = pj.max_ol(n_dist);
     ddm = -__dmul_rn(__dmul_rn((double)W, m.beta_d), (double)(ol_p < max_ol ? ol_p : max_ol));
     ddt = __dadd_rn(ddp, ddm);
   }
@@ -124,6 +130,24 @@ __device__ __forceinline__ void arrange(const rs_cost_model& m, bool prefill_fir
     else action = (ddt < 0) ? RS_ACTION_PREFILL : RS_ACTION_DECODE;
   }
 }
+
+struct OlProj {  // rs_arrange: terms from the sorted output limits
+  const long long* ol;
+  __device__ __forceinline__ double term(int i, double adn, long long ol_p) const {
+    return __dmul_rn(adn, (double)(ol[i] < ol_p ? ol[i] : ol_p));
+  }
+  __device__ __forceinline__ long long max_ol(int n) const {
+    long long x = 0;
+    for (int i = 0; i < n; ++i) x = ol[i] > x ? ol[i] : x;
+    return x;
+  }
+};
+struct TermProj {  // the engine: terms precomputed by the whole CTA (phase E)
+  const double* t;
+  long long mx;
+  __device__ __forceinline__ double term(int i, double, long long) const { return t[i]; }
+  __device__ __forceinline__ long long max_ol(int) const { return mx; }
+};
 
 // Parity mode: snapshot of this iteration's priority update into row `row`
 // (all threads): every admitted relQuery's priority and flags (estimated /
@@ -672,13 +696,21 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   const bool has_p = S.taken > 0, has_d = c.n_run > 0;
   const bool need_proj = (kC || !P.prefill_first) && has_p && has_d && S.dmin_slot != S.head && S.m_plus <= S.m_minus;
   if (need_proj) {
-    // distinct running relQueries sorted by rel_id (engine.py:406-408)
+    // distinct running relQueries in rel_id order (engine.py:406-408): each one's
+    // position and projection term (arranger.py:130-137), computed in parallel;
+    // thread 0 then only adds the terms in order
     const int nd = c.n_rrq;
+    const double adn = __dmul_rn(P.pol.alpha_d, (double)S.taken);
+    const long long olp = rq.ol[S.head];
     for (int i = tid; i < nd; i += kThreads) {
-      const int ri = rq.relrank[c.rrq[i]];
+      const int a = c.rrq[i];
+      const int ri = rq.relrank[a];
       int pos = 0;
+#pragma unroll 4
       for (int k = 0; k < nd; ++k) pos += rq.relrank[c.rrq[k]] < ri;
-      S.sorted_dist[pos] = c.rrq[i];
+      const long long o = rq.ol[a];
+      S.dterm[pos] = __dmul_rn(adn, (double)(o < olp ? o : olp));
+      atomicMax(&S.max_ol, (int)o);
     }
     if (tid == 0) S.n_dist = nd;
     __syncthreads();
@@ -686,10 +718,10 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   if (tid == 0) {
     int action, kase;
     double dp, dm, dt, mp, mmn;
-    const int* sd = S.sorted_dist;
     arrange(P.pol, !kC && P.prefill_first, P.force, has_p, has_d, S.dmin_slot == S.head, S.m_plus, S.m_minus, S.utok_sum,
-            S.taken, need_proj ? rq.ol[S.head] : 0, need_proj ? S.n_dist : 0, [&](int i) { return (long long)rq.ol[sd[i]]; },
+            S.taken, need_proj ? rq.ol[S.head] : 0, need_proj ? S.n_dist : 0, TermProj{S.dterm, (long long)S.max_ol},
             S.W, action, kase, mp, mmn, dp, dm, dt);
+    S.max_ol = 0;  // for the next projection
     S.action = action;
     c.zptr = zptr_new;
     if (z_cache) {  // valid until an admission or a prefill of that relQuery
@@ -773,6 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
     S.rq = rq_carve(rq_base, T.R);
     S.pf_head = -1;  // no previous head to prefetch for
     S.spec_ok = 0;   // the launch's first update runs in place (dpu_update)
+    S.max_ol = 0;
   }
   __syncthreads();
   if (S.c.status == RS_RUNNING) {
@@ -891,7 +924,7 @@ __global__ void arrange_kernel(int n_run, const long long* run_rel, const long l
   int action, kase;
   double mp, mmn, dp, dm, dt;
   arrange(m, prefill_first, force, n_p > 0, n_run > 0, n_run > 0 && n_p > 0 && d_min_rel == p_rel, m_plus, m_minus,
-          utok_sum, n_p, ol_p, n_run, [&](int i) { return sorted_ol[i]; }, W, action, kase, mp, mmn, dp, dm, dt);
+          utok_sum, n_p, ol_p, n_run, OlProj{sorted_ol}, W, action, kase, mp, mmn, dp, dm, dt);
   rs_iter_record r{};
   r.m_plus = mp;
   r.m_minus = mmn;

@@ -208,7 +208,8 @@ struct Shared {
   unsigned long long sh_key[32];  // sharded pool: the shards' waiting heads of this iteration
   int sh_idx[32];
   int n_dist, act_dirty, rrq_dirty;
-  int sorted_dist[kMaxRun];
+  double dterm[kMaxRun];  // projection terms of the distinct running relQueries, rel_id order
+  int max_ol;             // ... and their largest output limit (reset after each use)
   int cand_tok[kMaxRun];  // staged candidate prefill rows (tok, out)
   int cand_out[kMaxRun];
   int cand_u[kMaxRun];     // inclusive utok prefix of the candidate rows
