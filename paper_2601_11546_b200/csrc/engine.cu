@@ -961,86 +961,57 @@ __global__ void __launch_bounds__(kThreads) first_sight_kernel(int R, const int*
 }
 
 // First sight, segment-parallel (when PEM segments close by count only,
-// mns <= 256): one warp per PEM segment of every relQuery -- a whole-grid,
-// bandwidth-shaped pass that reads each row's tok once -- writes the
-// segment's terms in the reference's order (its prefill sub-batches, then the
-// decode term: pem(), priority.py:187-217, every row unprefilled with utok =
-// tok and remaining = output_limit); first_sight_sum_kernel then adds each
-// relQuery's terms in order.  seg[sg] = (first row, rows, output limit) of
-// segment sg (host-built).  Each warp walks its segments with the next
-// segment's tok already in flight (coalesced: lane l holds rows l, l+32, ...)
-// and its descriptor two ahead, so HBM latency hides behind the sub-batch
-// chain; the rows are transposed through shared memory (skewed against bank
-// conflicts) so that each lane scans 8 consecutive rows.
+// mns <= 256): a whole-grid, bandwidth-shaped pass that reads each row's tok
+// once.  One THREAD per PEM segment of every relQuery walks the segment's rows
+// in order -- pem()'s own scan (priority.py:187-217) with every row unprefilled,
+// utok = tok and remaining = output_limit: a prefill sub-batch closes before a
+// row that would take it past mnbt -- and writes the segment's terms in the
+// reference's order (its sub-batches, then the decode term);
+// first_sight_sum_kernel then adds each relQuery's terms in order.  A warp thus
+// advances 32 segments at once with a handful of instructions per row, instead
+// of one segment's sequential sub-batch chain per warp; each lane reads its rows
+// by whole cache lines, two lines in flight, so HBM sees every line once.
+// seg[sg] = (first row, rows, output limit) of segment sg (host-built).
 // Terms per segment are bounded by 2*sum(tok)/mnbt + 3 (consecutive next-fit
 // sub-batches exceed mnbt together); the host sizes `bound` from max(tok).
-__device__ __forceinline__ int fs_skew(int x) { return x + (x >> 5); }
-
-__global__ void __launch_bounds__(kThreads) first_sight_seg_kernel(int n_seg, const int4* seg, const int* tok,
-                                                                   PemModel m, int bound, double* terms, int* nterm) {
-  __shared__ int U[kWarps][kSmallMns + kSmallMns / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int* Uw = U[warp];
-  const int stride = gridDim.x * kWarps;
-  int sg = blockIdx.x * kWarps + warp;
-  int4 d_cur = sg < n_seg ? seg[sg] : make_int4(0, 0, 0, 0);
-  int4 d_nxt = sg + stride < n_seg ? seg[sg + stride] : make_int4(0, 0, 0, 0);
-  int nv[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) nv[i] = i * 32 + lane < d_cur.y ? tok[d_cur.x + i * 32 + lane] : 0;
-  for (; sg < n_seg; sg += stride) {
-    const int4 d = d_cur;
-    int cv[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) cv[i] = nv[i];
-    // next segment's rows in flight, the one after's descriptor too
-    d_cur = d_nxt;
-    d_nxt = sg + 2 * stride < n_seg ? seg[sg + 2 * stride] : make_int4(0, 0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) nv[i] = i * 32 + lane < d_cur.y ? tok[d_cur.x + i * 32 + lane] : 0;
-    const int nloc = d.y;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) Uw[fs_skew(i * 32 + lane)] = cv[i];
-    __syncwarp();
-    const int per = (nloc + 31) >> 5, x0 = lane * per;  // per <= 8
-    int uv[8], ls = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      uv[i] = (i < per && x0 + i < nloc) ? Uw[fs_skew(x0 + i)] : 0;
-      ls += uv[i];
-    }
-    int run = warp_incl_scan(ls) - ls;
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      run += uv[i];
-      if (i < per && x0 + i < nloc) Uw[fs_skew(x0 + i)] = run;
-    }
-    __syncwarp();
+__global__ void __launch_bounds__(256) first_sight_seg_kernel(int n_seg, const int4* seg, const int* tok, PemModel m,
+                                                              int bound, double* terms, int* nterm) {
+  const long long mnbt = m.mnbt;
+  for (int sg = blockIdx.x * blockDim.x + threadIdx.x; sg < n_seg; sg += gridDim.x * blockDim.x) {
+    const int4 d = seg[sg];
+    // rows [d.x, d.x + d.y) read by whole 128-byte lines (8 x 16 B in flight, the
+    // next line prefetched while this one is scanned); rows outside the segment
+    // read as utok 0, which pem() skips
+    const int lo = d.x & ~31, hi = d.x + d.y;
+    const int4* t4 = reinterpret_cast<const int4*>(tok + lo);
     double* tj = terms + (size_t)sg * bound;
-    int nt = 0, bb = 0;
-    while (bb < nloc) {  // the prefill sub-batch chain (see dpu_small)
-      const int before = bb ? Uw[fs_skew(bb - 1)] : 0;
-      const int ub = Uw[fs_skew(bb)];
-      const int thr = ub - before > m.mnbt ? ub : before + (int)m.mnbt;
-      int nb = nloc;
-      for (int b2 = bb + 1; b2 < nloc; b2 += 32) {
-        const unsigned mx = __ballot_sync(kFull, b2 + lane < nloc && Uw[fs_skew(b2 + lane)] > thr);
-        if (mx) {
-          nb = b2 + __ffs(mx) - 1;
-          break;
+    int nt = 0;
+    long long p = 0;  // p_utok; p > 0 <=> p_nonempty (every tok >= 1)
+    int4 cur[8], nxt[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cur[i] = lo + 4 * i < hi ? __ldg(t4 + i) : make_int4(0, 0, 0, 0);
+    for (int r0 = lo; r0 < hi; r0 += 32) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        nxt[i] = r0 + 32 + 4 * i < hi ? __ldg(t4 + ((r0 + 32 - lo) >> 2) + i) : make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int4 q = cur[i >> 2];
+        int u = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
+        u = (r0 + i >= d.x && r0 + i < hi) ? u : 0;
+        if (u > 0 && p > 0 && p + u > mnbt) {
+          tj[nt++] = lin(m.ap, (double)p, m.bp);
+          p = 0;
         }
+        p += u;
       }
-      if (lane == 0) tj[nt] = lin(m.ap, (double)(Uw[fs_skew(nb - 1)] - before), m.bp);
-      ++nt;
-      bb = nb;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
     }
-    if (lane == 0) {
-      const long long o = d.z;
-      tj[nt] = __dadd_rn(__dmul_rn(m.ad, (double)((long long)nloc * o)), __dmul_rn(m.bd, (double)o));
-      nterm[sg] = nt + 1;
-    }
-    __syncwarp();
+    if (p > 0) tj[nt++] = lin(m.ap, (double)p, m.bp);
+    const long long o = d.z;
+    tj[nt] = __dadd_rn(__dmul_rn(m.ad, (double)((long long)d.y * o)), __dmul_rn(m.bd, (double)o));
+    nterm[sg] = nt + 1;
   }
 }
 
@@ -1717,9 +1688,8 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
             return fail(RS_ENOMEM, "first-sight scratch");
           double* d_terms = (double*)scratch;
           int* d_nt = (int*)((char*)scratch + b_terms);
-          const int grid = (int)std::min<long long>((ns + kWarps - 1) / kWarps, 148 * 4);
-          if (ns > 0)
-            first_sight_seg_kernel<<<grid, kThreads>>>(ns, d_segd, tokp, m, (int)bound, d_terms, d_nt);
+          const int grid = (int)std::min<long long>((ns + 255) / 256, 148 * 8);
+          if (ns > 0) first_sight_seg_kernel<<<grid, 256>>>(ns, d_segd, tokp, m, (int)bound, d_terms, d_nt);
           first_sight_sum_kernel<<<(unsigned)std::min<long long>((Ri + 255) / 256, 148 * 4), 256>>>(
               Ri, d_segp, (int)bound, d_terms, d_nt, fsp);
           cudaFreeAsync(scratch, 0);
