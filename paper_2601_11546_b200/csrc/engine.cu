@@ -1409,7 +1409,9 @@ static size_t arena_need(const rs_trace_view& v, const rs_config* cfg, long long
                       4 * R + rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
                       (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
                       12 * (R + 1) + 8 + 24 * R /* static-order sort scratch */ +
-                      4 * (R + 1) /* first-sight segments */ + 44 * 256;
+                      4 * (R + 1) /* first-sight segments */ +
+                      16 * (R + N / (size_t)std::max<long long>(cfg->max_num_seqs, 1) + 1) /* ... their descriptors */ +
+                      45 * 256;
   return (need + 255) & ~(size_t)255;
 }
 
