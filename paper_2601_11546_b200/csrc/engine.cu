@@ -1360,6 +1360,7 @@ struct rs_engine {
   int shard_world = 1, shard_rank = 0;  // sharded pool (rs_engine_create_sharded); rank -1: all shards here
   ShardRec* mbox = nullptr;              // this engine's mailbox(es)
   ShardRec** d_peers = nullptr;          // device array [world] of peer mailbox pointers
+  bool mbox_pooled = false;              // mailboxes from the stream-ordered pool (all shards in this process)
   bool connected = true;                 // one-shard engines: peers' mailboxes known (rs_engine_connect)
   bool fast = true;  // every trace qualifies for engine_kernel<true, *>
   bool common = false;  // ... and the configuration is the common one (engine_kernel<true, true>)
@@ -2047,6 +2048,7 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
     else
       rc = build_trace(traces[t], cfg, *policy_model, rng[t], log_capacity, e->traces[t], shard_world, srank);
     if (rc) return bail(rc);
+    if (shard_world > 1) pc.mark(t == 0 ? "shard 0 built" : "replica cloned");
   }
   // shared memory: the control block etc., plus the relQuery table of every
   // trace whose table fits next to it (the others read theirs from HBM)
@@ -2062,11 +2064,16 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   bool all_deferred = shard_world == 1;
   for (auto& h : e->traces) all_deferred = all_deferred && h.deferred;
   if ((rc = finish_deferred(e, all_deferred))) return bail(rc);
+  pc.mark("deferred uploads");
   if (shard_world > 1) {  // mailboxes (shard.cuh); zeroed: sequence numbers start at 1
     const size_t mb = mailbox_bytes(shard_world);
     const int n_mb = shard_rank < 0 ? shard_world : 1;
-    if (cudaMalloc(&e->mbox, mb * n_mb) != cudaSuccess || cudaMemset(e->mbox, 0, mb * n_mb) != cudaSuccess ||
-        cudaMalloc(&e->d_peers, sizeof(ShardRec*) * shard_world) != cudaSuccess)
+    // one process: from the stream-ordered pool (a plain cudaMalloc here measured 3-30 ms next to
+    // torch's cached allocations); one shard per process: cudaMalloc, the mailbox is IPC-exported
+    e->mbox_pooled = shard_rank < 0;
+    const cudaError_t am = e->mbox_pooled ? cudaMallocAsync(&e->mbox, mb * n_mb, 0) : cudaMalloc(&e->mbox, mb * n_mb);
+    if (am != cudaSuccess || cudaMemsetAsync(e->mbox, 0, mb * n_mb, 0) != cudaSuccess ||
+        cudaMallocAsync(&e->d_peers, sizeof(ShardRec*) * shard_world, 0) != cudaSuccess)
       return bail(fail(RS_ENOMEM, "mailbox allocation failed"));
     std::vector<ShardRec*> peers(shard_world, nullptr);
     for (int d = 0; d < shard_world; ++d)
@@ -2584,8 +2591,8 @@ void rs_engine_destroy(rs_engine* e) {
     cudaEventSynchronize(e->ready);
     cudaEventDestroy(e->ready);
   }
-  if (e->mbox) cudaFree(e->mbox);
-  if (e->d_peers) cudaFree(e->d_peers);
+  if (e->mbox) e->mbox_pooled ? cudaFreeAsync(e->mbox, 0) : cudaFree(e->mbox);
+  if (e->d_peers) cudaFreeAsync(e->d_peers, 0);
   for (auto& h : e->traces) {
     for (void* p : h.allocs) cudaFree(p);
     if (h.arena_alloc) cudaFreeAsync(h.arena_alloc, 0);
