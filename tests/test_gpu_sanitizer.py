@@ -1,5 +1,7 @@
-"""compute-sanitizer racecheck / memcheck over short device runs (SURVEY 5:
-race detection).  Skipped when compute-sanitizer is not on PATH."""
+"""compute-sanitizer racecheck / memcheck / synccheck over short device runs (SURVEY 5:
+race detection): the general kernel (sp, finite tau, noise, a sharded pool) and the
+common-configuration kernel with its pipelined update.  Skipped when
+compute-sanitizer is not on PATH."""
 
 import os
 import shutil
@@ -17,6 +19,11 @@ import sys; sys.path.insert(0, {root!r})
 from paper_2601_11546_b200 import *
 from paper_2601_11546_b200.engine import Engine
 for policy, tc, kw in [("sp", dict(num_relqueries=40, size_range=(1, 40), rate=10.0, seed=36), {{}}),
+                       # the common-configuration kernel: the pipelined update (groups M and D, named
+                       # barriers, the arrive-only advance barrier and the join at the admission)
+                       ("relserve", dict(num_relqueries=30, size_range=(20, 300), rate=50.0, seed=5),
+                        dict(capacity_blocks=400)),
+                       ("relserve-dp", dict(num_relqueries=25, size_range=(1, 200), rate=50.0, seed=6), {{}}),
                        ("relserve", dict(num_relqueries=30, size_range=(1, 60), rate=5.0, seed=3),
                         dict(capacity_blocks=120, tau=0.2))]:
     t = generate_trace(TraceConfig(**tc))
