@@ -307,6 +307,56 @@ __device__ __forceinline__ void exec_done_arrive() {  // group M
 __device__ __forceinline__ void exec_done_wait() {  // group D
   asm volatile("bar.sync %0, %1;" ::"n"(kBarExecDone), "n"(kThreads) : "memory");
 }
+constexpr int kBarDecision = 6;  // group M has decided the iteration's action (S.action, S.head, S.taken)
+__device__ __forceinline__ void decision_arrive() {  // group M
+  asm volatile("bar.arrive %0, %1;" ::"n"(kBarDecision), "n"(kThreads) : "memory");
+}
+__device__ __forceinline__ void decision_wait() {  // group D
+  asm volatile("bar.sync %0, %1;" ::"n"(kBarDecision), "n"(kThreads) : "memory");
+}
+
+// block_count_argmin over the G::kN threads of a group (its warps consecutive from warp 0)
+template <class G>
+__device__ __forceinline__ void group_count_argmin(int& cnt, unsigned long long& key, int& idx, RedSmem& sm) {
+  if constexpr (G::kN == kThreads) {
+    block_count_argmin(cnt, key, idx, sm);
+  } else {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(kFull, key, d);
+      const int oi = __shfl_xor_sync(kFull, idx, d);
+      cnt += __shfl_xor_sync(kFull, cnt, d);
+      if (ok < key || (ok == key && oi < idx)) {
+        key = ok;
+        idx = oi;
+      }
+    }
+    if (lane == 0) {
+      sm.k[warp] = key;
+      sm.i[warp] = idx;
+      sm.n[warp] = cnt;
+    }
+    G::sync();
+    unsigned long long k = lane < G::kW ? sm.k[lane] : ~0ULL;
+    int i = lane < G::kW ? sm.i[lane] : 0x7FFFFFFF;
+    int n = lane < G::kW ? sm.n[lane] : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(kFull, k, d);
+      const int oi = __shfl_xor_sync(kFull, i, d);
+      n += __shfl_xor_sync(kFull, n, d);
+      if (ok < k || (ok == k && oi < i)) {
+        k = ok;
+        i = oi;
+      }
+    }
+    G::sync();
+    key = k;
+    idx = i;
+    cnt = n;
+  }
+}
 
 // block_scan32 over the G::kN threads of a group (thread index within the group
 // = threadIdx.x - base; the group's warps are consecutive)

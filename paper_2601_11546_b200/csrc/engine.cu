@@ -36,6 +36,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/relserve.h"
@@ -482,6 +483,34 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   }
   phase_mark(c, 1);
 
+  // kC: group D leaves the iteration here.  The waiting order, the candidates
+  // and the decision run on group M alone; group D computes the next
+  // iteration's update from the state this iteration's action will leave --
+  // at once when the action is already certain (a decode forced by a full
+  // running set or an empty waiting queue: no prefill candidate can exist,
+  // arranger.py:80-112, 146-179), else once group M has decided (kBarDecision).
+  const bool early = c.n_run > 0 && (c.n_run >= cfg.max_num_seqs || c.n_wait == 0);
+  if constexpr (kC) {
+    if (opaque_warp() >= kMWarps) {
+      if (T.snap_prio) record_parity(P, T, S, c.n_log & (T.log_cap - 1));  // meets group M's call (whole CTA)
+      const bool allowed = !last && c.iteration + 1 < cfg.iteration_limit;
+      int action = RS_ACTION_DECODE, h = -1, nh = 0;
+      if (!early) {
+        decision_wait();
+        action = S.action;
+        h = S.head;
+        nh = S.taken;
+      }
+      dpu_spec(P, T, S, action, h, nh, allowed);
+      exec_done_wait();
+      if (opaque_warp() == kMWarps) spec_commit(S, T);
+      return S.go_exec;
+    }
+  }
+  // the threads and barrier of phases C-E: the whole CTA, or group M (kC)
+  using GC = typename std::conditional<kC, GM, GAll>::type;
+  constexpr int NT = GC::kN;
+
   // ---- C: waiting head = argmin (prio, rank) over relQueries with pending
   // rows, and W = len(waiting) (engine.py:277-281).  A relQuery none of whose
   // rows was prefilled keeps a static priority (first-sight estimate reused,
@@ -581,7 +610,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       int w = 0;
       key = ~0ULL;
       idx = 0x7FFFFFFF;
-      for (int a = tid; a < c.n_admitted; a += kThreads) {
+      for (int a = tid; a < c.n_admitted; a += NT) {
         if (rq.q[a] < rq.off[a + 1] - rq.off[a] && (T.shard_world == 1 || a % T.shard_world == T.shard_rank)) {
           ++w;
           const unsigned long long k = okey(rq.prio[a]);
@@ -591,7 +620,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
           }
         }
       }
-      block_count_argmin(w, key, idx, S.red);  // result is block-uniform in registers
+      group_count_argmin<GC>(w, key, idx, S.red);  // result is group-uniform in registers
     }
     if (!kC && T.shard_world > 1) {  // allgather of the shards' heads and priorities
       if (!shard_exchange(T, S, key, idx)) return false;
@@ -654,7 +683,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     }
     const long long headroom = cfg.cap - c.kv;
     int cu = 0, ck = 0;
-    for (int base = 0; base < J; base += kThreads) {
+    for (int base = 0; base < J; base += NT) {
       const int j = base + tid;
       int v[2] = {0, 0};
       if (j < J) {
@@ -665,7 +694,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
         v[1] = t + olh;  // kv need
       }
       int tot[2];
-      block_scan32<2>(v, S.s32, tot);
+      group_scan32<GC, 2>(v, S.s32, tot, tid >> 5);
       bool bad = false;
       if (j < J) {
         const int U = cu + v[0], K = ck + v[1];
@@ -676,19 +705,19 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       if (m && (tid & 31) == 0) atomicMin(&S.first_bad, base + (tid & ~31) + __ffs(m) - 1);
       cu += tot[0];
       ck += tot[1];
-      __syncthreads();
+      GC::sync();
       if (S.first_bad < J) break;
     }
     if (tid == 0) {
       const int taken = S.first_bad < J ? S.first_bad : J;
-      const int loaded = ((S.first_bad < J ? S.first_bad : J - 1) / kThreads + 1) * kThreads;
+      const int loaded = ((S.first_bad < J ? S.first_bad : J - 1) / NT + 1) * NT;
       c.alg_bytes += 8LL * (J < loaded ? J : loaded);  // candidate tok + out
       S.taken = taken;
       S.cand_mh = mh;
       S.utok_sum = taken > 0 ? S.cand_u[taken - 1] : 0;
       S.m_minus = taken > 0 ? rq.prio[h] : qnan();
     }
-    __syncthreads();
+    GC::sync();
     phase_mark(c, 12);
   }
 
@@ -702,7 +731,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     const int nd = c.n_rrq;
     const double adn = __dmul_rn(P.pol.alpha_d, (double)S.taken);
     const long long olp = rq.ol[S.head];
-    for (int i = tid; i < nd; i += kThreads) {
+    for (int i = tid; i < nd; i += NT) {
       const int a = c.rrq[i];
       const int ri = rq.relrank[a];
       int pos = 0;
@@ -713,7 +742,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       atomicMax(&S.max_ol, (int)o);
     }
     if (tid == 0) S.n_dist = nd;
-    __syncthreads();
+    GC::sync();
   }
   if (tid == 0) {
     int action, kase;
@@ -750,7 +779,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       r.kv_reserved = 0;
     }
   }
-  __syncthreads();
+  GC::sync();
   const int action = S.action;
   phase_mark(c, 3);
 
@@ -758,23 +787,17 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   if constexpr (kC) {
     // pipelined: group M executes this iteration while group D computes the
     // next iteration's priority update of the partially prefilled relQueries
-    // (dpu_spec) from the state this advance leaves; both join at the barrier
+    // (dpu_spec, started after phase B) from the state this advance leaves.
     // The groups do not join here: group M signals the advance done (barrier
     // kBarExecDone, arrive only) and goes on to the next iteration's admission;
     // group D, once its update is computed, waits for that signal, commits the
     // update against the advance's result, and both meet at the admission
     // barrier -- so the update may run over into the admission.
-    const bool allowed = !last && c.iteration + 1 < cfg.iteration_limit;
-    if (opaque_warp() < kMWarps) {
-      const bool go = execute<kC, GM, true>(P, T, S, action);  // group-uniform
-      if (tid == 0) S.go_exec = go;
-      exec_done_arrive();
-      return go;
-    }
-    dpu_spec(P, T, S, action, S.head, S.taken, allowed);
-    exec_done_wait();
-    if (opaque_warp() == kMWarps) spec_commit(S, T);
-    return S.go_exec;
+    if (!early) decision_arrive();  // group D (waiting since phase B) may start the update
+    const bool go = execute<kC, GM, true>(P, T, S, action);  // group-uniform
+    if (tid == 0) S.go_exec = go;
+    exec_done_arrive();
+    return go;
   } else {
     return execute<kC, GAll, false>(P, T, S, action);
   }
