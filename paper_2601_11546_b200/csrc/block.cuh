@@ -307,7 +307,7 @@ __device__ __forceinline__ void exec_done_arrive() {  // group M
 __device__ __forceinline__ void exec_done_wait() {  // group D
   asm volatile("bar.sync %0, %1;" ::"n"(kBarExecDone), "n"(kThreads) : "memory");
 }
-constexpr int kBarDecision = 6;  // group M has decided the iteration's action (S.action, S.head, S.taken)
+constexpr int kBarDecision = 6;  // group M has the candidates (S.head, S.taken): group D may start the update
 __device__ __forceinline__ void decision_arrive() {  // group M
   asm volatile("bar.arrive %0, %1;" ::"n"(kBarDecision), "n"(kThreads) : "memory");
 }

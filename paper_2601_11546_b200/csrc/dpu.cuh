@@ -849,7 +849,8 @@ __device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const int lane = threadIdx.x & 31;
-  bool ok = S.spec_valid && S.go_exec;  // (c.status may change concurrently: the next admission)
+  // (c.status may change concurrently: the next admission); a speculated action must be phase E's
+  bool ok = S.spec_valid && S.go_exec && S.spec_action == S.action;
   const int n = S.spec_n;
   bool keep = false, bad = false;
   int a = 0;

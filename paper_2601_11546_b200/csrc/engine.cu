@@ -495,12 +495,13 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       if (T.snap_prio) record_parity(P, T, S, c.n_log & (T.log_cap - 1));  // meets group M's call (whole CTA)
       const bool allowed = !last && c.iteration + 1 < cfg.iteration_limit;
       int action = RS_ACTION_DECODE, h = -1, nh = 0;
-      if (!early) {
-        decision_wait();
-        action = S.action;
-        h = S.head;
-        nh = S.taken;
+      if (!early) {  // once the candidates are known: no prefill candidate decides the action
+        decision_wait();  // (decode, or idle); otherwise speculate the prefill, which every
+        h = S.head;       // non-forced decision at configs 2, 3 and 5 is -- spec_commit
+        nh = S.taken;     // discards the update if phase E decided otherwise
+        action = nh > 0 ? RS_ACTION_PREFILL : c.n_run > 0 ? RS_ACTION_DECODE : RS_ACTION_IDLE;
       }
+      if ((threadIdx.x & 31) == 0 && opaque_warp() == kMWarps) S.spec_action = action;
       dpu_spec(P, T, S, action, h, nh, allowed);
       exec_done_wait();
       if (opaque_warp() == kMWarps) spec_commit(S, T);
@@ -720,6 +721,9 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     GC::sync();
     phase_mark(c, 12);
   }
+  if constexpr (kC) {
+    if (!early) decision_arrive();  // the candidates: group D may start the update (see above)
+  }
 
   // ---- E: decision (engine.py:387-433, arranger.py:115-179)
   const bool has_p = S.taken > 0, has_d = c.n_run > 0;
@@ -793,7 +797,6 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     // group D, once its update is computed, waits for that signal, commits the
     // update against the advance's result, and both meet at the admission
     // barrier -- so the update may run over into the admission.
-    if (!early) decision_arrive();  // group D (waiting since phase B) may start the update
     const bool go = execute<kC, GM, true>(P, T, S, action);  // group-uniform
     if (tid == 0) S.go_exec = go;
     exec_done_arrive();

@@ -229,6 +229,7 @@ struct Shared {
   // iteration's state advance (dpu.cuh dpu_spec); committed after the join
   int spec_ok;    // this iteration's update of c.act is already done (committed)
   int spec_valid; // group D's verdict on its result (fits the fast path, no Lemire rejection)
+  int spec_action; // the action the update assumed (certain, or the speculated prefill)
   int spec_n;     // entries of the speculative list
   int spec_rank[kSmallEst];
   int spec_m[kSmallEst];     // chain length its ratio assumed (checked against the advance's)
