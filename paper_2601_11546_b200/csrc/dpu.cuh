@@ -851,6 +851,9 @@ __device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
   const int lane = threadIdx.x & 31;
   // (c.status may change concurrently: the next admission); a speculated action must be phase E's
   bool ok = S.spec_valid && S.go_exec && S.spec_action == S.action;
+#ifdef RS_COUNT_MISSPEC  // experiment: count discarded speculations (phase slot 20)
+  if (lane == 0 && S.spec_valid && S.go_exec && S.spec_action != S.action) c.phase[20] += 1;
+#endif
   const int n = S.spec_n;
   bool keep = false, bad = false;
   int a = 0;

@@ -495,11 +495,17 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       if (T.snap_prio) record_parity(P, T, S, c.n_log & (T.log_cap - 1));  // meets group M's call (whole CTA)
       const bool allowed = !last && c.iteration + 1 < cfg.iteration_limit;
       int action = RS_ACTION_DECODE, h = -1, nh = 0;
-      if (!early) {  // once the candidates are known: no prefill candidate decides the action
-        decision_wait();  // (decode, or idle); otherwise speculate the prefill, which every
-        h = S.head;       // non-forced decision at configs 2, 3 and 5 is -- spec_commit
-        nh = S.taken;     // discards the update if phase E decided otherwise
-        action = nh > 0 ? RS_ACTION_PREFILL : c.n_run > 0 ? RS_ACTION_DECODE : RS_ACTION_IDLE;
+      if (!early) {  // once the candidates are known, decide_next (arranger.py:146-179) as far as
+        decision_wait();  // it goes without the Delta projection: no prefill candidate -> decode (or
+        h = S.head;       // idle); internal or preemption -> prefill; transitional: forced by the
+        nh = S.taken;     // policy, else the prefill is speculated (spec_commit discards the update
+        if (nh == 0) {    // if phase E decided otherwise; never at configs 2, 3 and 5)
+          action = c.n_run > 0 ? RS_ACTION_DECODE : RS_ACTION_IDLE;
+        } else if (c.n_run == 0 || S.dmin_slot == h || S.m_plus > S.m_minus) {
+          action = RS_ACTION_PREFILL;
+        } else {
+          action = P.force == 2 ? RS_ACTION_DECODE : RS_ACTION_PREFILL;
+        }
       }
       if ((threadIdx.x & 31) == 0 && opaque_warp() == kMWarps) S.spec_action = action;
       dpu_spec(P, T, S, action, h, nh, allowed);

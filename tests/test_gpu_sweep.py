@@ -35,13 +35,32 @@ def _case(i):
     return tc, cons, kw, policy, MODELS[int(r.integers(0, 3))], int(r.integers(0, 100)), shards
 
 
+def _common_case(i):
+    """The common configuration (relsim's default EngineConfig with a DPU policy, one shard:
+    the specialised kernel with the pipelined update and its speculation) on random traces
+    and constraints."""
+    tc, cons, kw, policy, model, seed, _ = _case(500 + i)
+    kw = dict(capacity_blocks=kw["capacity_blocks"])
+    policy = ("relserve", "relserve-pp", "relserve-dp")[i % 3]
+    return tc, cons, kw, policy, model, seed, 1
+
+
 @pytest.mark.parametrize("i", range(120))
 def test_random_sweep_device_equals_oracle(i, oracle_mod):
+    _sweep_case(_case(i), oracle_mod)
+
+
+@pytest.mark.parametrize("i", range(60))
+def test_random_sweep_common_kernel_equals_oracle(i, oracle_mod):
+    _sweep_case(_common_case(i), oracle_mod)
+
+
+def _sweep_case(case, oracle_mod):
     from paper_2601_11546_b200 import EngineConfig, SchedulerConstraints, TraceConfig, generate_trace, world_preset
     from paper_2601_11546_b200.engine import Engine
     from paper_2601_11546_b200.priority import InfeasibleRequestError
 
-    tc, cons, kw, policy, model, seed, shards = _case(i)
+    tc, cons, kw, policy, model, seed, shards = case
     trace = generate_trace(TraceConfig(**tc))
     cfg = EngineConfig(constraints=SchedulerConstraints(*cons), iteration_limit=20_000, **kw)
     w = world_preset(model)
