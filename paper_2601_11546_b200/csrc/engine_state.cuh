@@ -36,8 +36,8 @@ constexpr int kPhases = 24;
 constexpr int kSmallEst = 32;   // DPU fast path: at most this many re-estimated relQueries
 constexpr int kSmallMns = 256;  // ... and max_num_seqs at most this
 constexpr int kMaxJobs = 64;    // ... and at most this many PEM segments
-constexpr int kJobTerms = 32;
-constexpr int kZScanRounds = 8;  // static-order scan: 32-entry rounds before the full reduction   // fp64 terms per segment kept in shared memory (rest spill to HBM)
+constexpr int kJobTerms = 32;   // fp64 terms per PEM segment kept in shared memory (the rest spill to HBM)
+constexpr int kZScanRounds = 8;  // static-order scan: 32-entry rounds before the full reduction
 
 struct FifoEnt {
   unsigned long long t0;  // touch time of the tail's first block
