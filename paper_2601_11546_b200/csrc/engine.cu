@@ -632,6 +632,16 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     if (!kC && T.shard_world > 1) {  // allgather of the shards' heads and priorities
       if (!shard_exchange(T, S, key, idx)) return false;
     }
+    if (kC && T.shard_world > 1) {  // every shard has every priority: only the heads travel
+      if (!shard_exchange_heads<GC>(T, S, key, idx)) {
+        if constexpr (kC) {  // release group D (waiting for the candidates or the advance)
+          if (tid == 0) S.go_exec = 0;
+          if (!early) decision_arrive();
+          exec_done_arrive();
+        }
+        return false;
+      }
+    }
     head_l = c.n_wait > 0 && idx != 0x7FFFFFFF ? idx : -1;
     if (tid == 0) {
       if (c.n_wait > 0 && head_l < 0) {  // internal inconsistency: never expected
@@ -2136,8 +2146,8 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   e->fast = true;
   for (auto& h : e->traces) e->fast = e->fast && h.dev.fast;
   // the common configuration's specialised kernel (see iterate)
-  e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) &&
-              shard_world == 1 && cfg->log_decisions && cfg->block_size == 16 && cfg->sample_size == 8;
+  e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && cfg->log_decisions &&
+              cfg->block_size == 16 && cfg->sample_size == 8;
   for (auto& h : e->traces) e->common = e->common && h.dev.log_cap > 0;
   cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
   if (ce == cudaSuccess)

@@ -139,4 +139,59 @@ __device__ bool shard_exchange(const TraceDev& T, Shared& S, unsigned long long&
   return true;
 }
 
+// The common-configuration kernel's exchange (group G = group M): every shard
+// computes the update of every partially prefilled relQuery itself (the update
+// is pipelined off the critical path, so replicating it is cheaper than
+// exchanging its results), so only the local waiting heads travel: three
+// flagged words per shard.  Same mailboxes, flags and parity as shard_exchange.
+template <class G>
+__device__ bool shard_exchange_heads(const TraceDev& T, Shared& S, unsigned long long& key, int& idx) {
+  Ctl& c = S.c;
+  const int W = T.shard_world, me = T.shard_rank;
+  const int tid = threadIdx.x;
+  const unsigned flag = (unsigned)(c.iteration + 1);
+  const int par = (int)(c.iteration & 1);
+  if (tid < W && tid != me) {
+    unsigned long long* w = T.peers[tid][2 * me + par].w;
+    ll_store(w + 0, flag, (unsigned)key);
+    ll_store(w + 1, flag, (unsigned)(key >> 32));
+    ll_store(w + 2, flag, (unsigned)idx);
+  }
+  if (tid == 0) S.go = 1;
+  bool ok = true;
+  if (tid < W) {
+    unsigned long long k = ~0ULL;
+    int i = 0x7FFFFFFF;
+    if (tid != me) {
+      const unsigned long long* w = T.self_mbox[2 * tid + par].w;
+      unsigned lo = 0, hi = 0, ix = 0;
+      ok = ll_load(w, flag, lo) && ll_load(w + 1, flag, hi) && ll_load(w + 2, flag, ix);
+      k = ((unsigned long long)hi << 32) | lo;
+      i = (int)ix;
+    }
+    S.sh_key[tid] = k;
+    S.sh_idx[tid] = i;
+  }
+  G::sync();
+  if (!ok) S.go = 0;
+  G::sync();
+  if (!S.go) {
+    if (tid == 0) {
+      c.status = RS_ECUDA;
+      c.error_detail = 10;
+    }
+    return false;
+  }
+  for (int s = 0; s < W; ++s) {
+    const unsigned long long k = S.sh_key[s];
+    const int i = S.sh_idx[s];
+    if (s != me && (k < key || (k == key && i < idx))) {
+      key = k;
+      idx = i;
+    }
+  }
+  if (tid == 0) c.alg_bytes += 24LL * W;  // records received
+  return true;
+}
+
 }  // namespace rsd
