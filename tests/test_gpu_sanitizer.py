@@ -33,6 +33,15 @@ for policy, tc, kw in [("sp", dict(num_relqueries=40, size_range=(1, 40), rate=1
     except SimulationAborted:
         pass
     e.close()
+# sharded pool on the common-configuration kernel (heads-only exchange, pipelined update)
+t = generate_trace(TraceConfig(num_relqueries=40, size_range=(20, 200), rate=50.0, seed=9))
+e = Engine(t, "relserve", world_preset("opt-13b-like"), EngineConfig(iteration_limit=80, capacity_blocks=300),
+           shards=3)
+try:
+    e.run()
+except SimulationAborted:
+    pass
+e.close()
 # sharded pool (3 shards as CTAs of one launch) with world-model noise
 t = generate_trace(TraceConfig(num_relqueries=60, size_range=(1, 50), rate=6.0, seed=8))
 e = Engine(t, "relserve", world_preset("llama-70b-like"), EngineConfig(iteration_limit=80, noise_sigma=0.2),
