@@ -1016,19 +1016,38 @@ __global__ void __launch_bounds__(kThreads) first_sight_kernel(int R, const int*
 // seg[sg] = (first row, rows, output limit) of segment sg (host-built).
 // Terms per segment are bounded by 2*sum(tok)/mnbt + 3 (consecutive next-fit
 // sub-batches exceed mnbt together); the host sizes `bound` from max(tok).
+// One 32-row line of a segment's scan: rows outside [vlo, vhi) of the line are
+// another segment's and are skipped (kMask: the line may hold such rows).
+template <bool kMask>
+__device__ __forceinline__ void fs_scan_line(const int4 (&q)[8], int vlo, int vhi, int mnbt, int& p, int& nt,
+                                             double* tj, const PemModel& m) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int4 v = q[i >> 2];
+    int u = (i & 3) == 0 ? v.x : (i & 3) == 1 ? v.y : (i & 3) == 2 ? v.z : v.w;
+    if (kMask) u = (i >= vlo && i < vhi) ? u : 0;
+    const int np = p + u;  // every row has tok >= 1: p > 0 <=> the sub-batch is non-empty
+    if (np > mnbt && p > 0 && u > 0) {  // the row would take the sub-batch past mnbt (priority.py:205-208)
+      tj[nt++] = lin(m.ap, (double)p, m.bp);
+      p = u;
+    } else {
+      p = np;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) first_sight_seg_kernel(int n_seg, const int4* seg, const int* tok, PemModel m,
                                                               int bound, double* terms, int* nterm) {
-  const long long mnbt = m.mnbt;
+  const int mnbt = (int)m.mnbt;
   for (int sg = blockIdx.x * blockDim.x + threadIdx.x; sg < n_seg; sg += gridDim.x * blockDim.x) {
     const int4 d = seg[sg];
     // rows [d.x, d.x + d.y) read by whole 128-byte lines (8 x 16 B in flight, the
-    // next line prefetched while this one is scanned); rows outside the segment
-    // read as utok 0, which pem() skips
+    // next line prefetched while this one is scanned); only the first and last
+    // lines can hold other segments' rows
     const int lo = d.x & ~31, hi = d.x + d.y;
     const int4* t4 = reinterpret_cast<const int4*>(tok + lo);
     double* tj = terms + (size_t)sg * bound;
-    int nt = 0;
-    long long p = 0;  // p_utok; p > 0 <=> p_nonempty (every tok >= 1)
+    int nt = 0, p = 0;  // p = p_utok of pem()
     int4 cur[8], nxt[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) cur[i] = lo + 4 * i < hi ? __ldg(t4 + i) : make_int4(0, 0, 0, 0);
@@ -1036,17 +1055,8 @@ __global__ void __launch_bounds__(256) first_sight_seg_kernel(int n_seg, const i
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         nxt[i] = r0 + 32 + 4 * i < hi ? __ldg(t4 + ((r0 + 32 - lo) >> 2) + i) : make_int4(0, 0, 0, 0);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int4 q = cur[i >> 2];
-        int u = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
-        u = (r0 + i >= d.x && r0 + i < hi) ? u : 0;
-        if (u > 0 && p > 0 && p + u > mnbt) {
-          tj[nt++] = lin(m.ap, (double)p, m.bp);
-          p = 0;
-        }
-        p += u;
-      }
+      if (r0 >= d.x && r0 + 32 <= hi) fs_scan_line<false>(cur, 0, 32, mnbt, p, nt, tj, m);
+      else fs_scan_line<true>(cur, d.x - r0, hi - r0, mnbt, p, nt, tj, m);
 #pragma unroll
       for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
     }
