@@ -45,7 +45,14 @@ def main():
                 rec = {"raises": type(e).__name__, "message": str(e)}
             out[f"{name}/{pol}"] = rec
             print(name, pol, rec.get("raises") or (rec["iterations"], rec["clock"]))
-    (ROOT / "tests" / "golden" / "edge" / "edge_cases.json").write_text(json.dumps(out, indent=0) + "\n")
+    _write(out)
+
+
+def _write(out):
+    import gzip
+
+    with gzip.open(ROOT / "tests" / "golden" / "edge" / "edge_cases.json.gz", "wt") as f:
+        json.dump(out, f)
 
 
 if __name__ == "__main__":

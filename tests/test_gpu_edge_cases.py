@@ -4,6 +4,7 @@ aborts), a request using exactly the whole KV budget and one over it, a row long
 than max_num_batched_tokens, a ragged burst with more rows than max_num_seqs, and
 all-tied arrivals ordered by rel_id -- every policy, on the device and on the oracle."""
 
+import gzip
 import json
 
 import pytest
@@ -14,7 +15,8 @@ from paper_2601_11546_b200 import (ArrivalTrace, InfeasibleRequestError, RelQuer
                                    SimulationAborted, world_preset)
 from paper_2601_11546_b200.engine import EngineConfig, run
 
-GOLD = json.loads((GOLDEN_DIR / "edge" / "edge_cases.json").read_text())
+with gzip.open(GOLDEN_DIR / "edge" / "edge_cases.json.gz", "rt") as _f:
+    GOLD = json.load(_f)
 KEYS = sorted(GOLD)
 ERRORS = {"SimulationAborted": SimulationAborted, "InfeasibleRequestError": InfeasibleRequestError}
 
