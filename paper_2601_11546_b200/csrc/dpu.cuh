@@ -64,7 +64,8 @@ struct PrioOut {
 
 // Sequential sample_cache_miss_ratio (prefix_cache.py:141-169) for relQuery a
 // (thread 0; the fallback after a Lemire rejection).
-__device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq, const Params& P, int a) {
+__device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq, const Params& P, int a,
+                                   uint32_t* idx) {
   const int off = rq.off[a];
   const int size = rq.off[a + 1] - off;
   const int q = rq.q[a];
@@ -73,8 +74,7 @@ __device__ double sample_ratio_seq(Pcg64& g, const TraceDev& T, const RqView& rq
   const long long mh = P.cfg.block_size * (long long)rq.m[a];
   const int k = (int)(P.cfg.sample_size < n ? P.cfg.sample_size : n);
   long long usum = 0, tsum = 0;
-  if (k < n) {
-    uint32_t idx[kMaxSample];
+  if (k < n) {  // idx: shared scratch (a local array would give the kernel a stack frame)
     choice_floyd(g, (uint32_t)n, (uint32_t)k, idx);
     for (int i = 0; i < k; ++i) {
       const long long t = T.tok[off + q + (int)idx[i]];
@@ -100,7 +100,7 @@ __device__ void ratios_sequential(const Params& P, const TraceDev& T, Shared& S,
   for (int e = 0; e < n_est; ++e) {
     const int ge = e0 + e;
     const int ae = ge < n_act ? c.act[ge] : S.new_lo + (ge - n_act);
-    S.est_ratio[e] = sample_ratio_seq(g, T, S.rq, P, ae);
+    S.est_ratio[e] = sample_ratio_seq(g, T, S.rq, P, ae, S.floyd_idx);
   }
   c.rng = g.to();
 }
@@ -816,11 +816,8 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   dphase_mark(c, 13);
   if (gw == 0 && lane < n_est && S.spec_jobs <= kMaxJobs) {  // ordered sums, entry by entry, in the reference's order
     double total = 0.0;
-    int cnt[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) cnt[u] = u < nj ? S.small.nterm[jo + u] : 0;
     for (int j = jo; j < jo + nj; ++j) {
-      const int cj = j - jo < 4 ? cnt[j - jo] : S.small.nterm[j];
+      const int cj = S.small.nterm[j];
       const double* tj = S.small.terms + j * kJobTerms;
       const int nsm = cj < kJobTerms ? cj : kJobTerms;
       int i = 0;
@@ -979,8 +976,7 @@ __device__ void first_sight(const Params& P, const TraceDev& T, Shared& S, int l
         else r = mid;
       }
       Pcg64 g = Pcg64::from(advance32(c.rng, T.fs_doff[l] - P0, S.jt));
-      uint32_t idx[kMaxSample];
-      choice_floyd(g, (uint32_t)(rq.off[l + 1] - rq.off[l]), (uint32_t)Ssz, idx);
+      choice_floyd(g, (uint32_t)(rq.off[l + 1] - rq.off[l]), (uint32_t)Ssz, S.floyd_idx);
       c.rng = g.to();
       S.new_lo_rs = l + 1;
     }
@@ -1121,7 +1117,7 @@ __device__ void dpu_batched(const Params& P, const TraceDev& T, Shared& S, const
     if (S.rng_reject) {  // a rejection shifts the stream: replay this batch sequentially
       if (tid == 0) {
         Pcg64 g = Pcg64::from(c.rng);
-        for (int e = 0; e < nb; ++e) S.est_ratio[e] = sample_ratio_seq(g, T, rq, P, S.est_rank[e]);
+        for (int e = 0; e < nb; ++e) S.est_ratio[e] = sample_ratio_seq(g, T, rq, P, S.est_rank[e], S.floyd_idx);
         c.rng = g.to();
       }
     } else {

@@ -222,6 +222,7 @@ struct Shared {
   double est_ratio[kEstBatch];
   PrefixSummary est_ps[kEstBatch];
   int rng_reject;
+  uint32_t floyd_idx[kMaxSample];  // thread 0's sequential numpy choice() replays (cold paths)
   unsigned long long rej_pos;  // first-sight replay: first stream position with a Lemire rejection
   int new_lo_rs;               // ... and the arrival its parallel replay restarts at
   // pipelined priority update (common configuration): group D computes the next
