@@ -488,7 +488,8 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   // iteration's update from the state this iteration's action will leave --
   // at once when the action is already certain (a decode forced by a full
   // running set or an empty waiting queue: no prefill candidate can exist,
-  // arranger.py:80-112, 146-179), else once group M has decided (kBarDecision).
+  // arranger.py:80-112, 146-179), else once group M has the candidates
+  // (kBarDecision).
   const bool early = c.n_run > 0 && (c.n_run >= cfg.max_num_seqs || c.n_wait == 0);
   if constexpr (kC) {
     if (opaque_warp() >= kMWarps) {
