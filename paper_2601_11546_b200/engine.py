@@ -537,6 +537,46 @@ class Engine:
         khz = _native.device_clock_khz(self.device)
         return sum(int(st.phase_cycles[k]) for k in phases) / (khz * 1e3) if khz else 0.0
 
+    def _admitted(self) -> np.ndarray:
+        """Trace indices of the admitted relQueries in admission order (engine.py:211-213, 243-269)."""
+        c = self.trace.columns()
+        n_adm = int(self._status.admitted) if self._status is not None else 0
+        return np.lexsort((c.rel_id, c.arrival))[:n_adm]
+
+    @property
+    def ledgers(self) -> dict:
+        """relsim's ``Engine.ledgers`` (engine.py:207, 258-262) between steps: a TimestampLedger per
+        admitted relQuery, in admission order, read from the device."""
+        c = self.trace.columns()
+        arrival, fps, lpe, lde = self._native.read_ledgers(0, c.num_relqueries)
+        rid = c.rel_id
+        nn = lambda x: None if x != x else float(x)  # noqa: E731  (NaN: unset)
+        return {int(rid[i]): TimestampLedger(float(arrival[i]), nn(fps[i]), nn(lpe[i]), nn(lde[i]))
+                for i in self._admitted().tolist()}
+
+    @property
+    def live_relqueries(self) -> dict:
+        """relsim's ``Engine.live_relqueries`` (engine.py:208, 254, 362) between steps: the admitted
+        relQueries with a request not yet done, in admission order (a relQuery without requests
+        stays live, as in the reference)."""
+        c = self.trace.columns()
+        _, _, comp, _ = self._native.read_requests(0, c.num_requests)
+        finished = comp >= 0
+        sizes = np.diff(c.row_off)
+        done_rows = np.zeros(c.num_relqueries, np.int64)
+        rq_of_row = np.repeat(np.arange(c.num_relqueries), sizes)
+        np.add.at(done_rows, rq_of_row[finished], 1)
+        entries = self.trace.entries
+        return {int(c.rel_id[i]): entries[i] for i in self._admitted().tolist()
+                if sizes[i] == 0 or done_rows[i] < sizes[i]}
+
+    @property
+    def decision_log(self) -> list:
+        """relsim's ``Engine.decision_log`` (engine.py:209, 419-433): the entries of the iterations
+        run so far."""
+        recs = np.concatenate(self._records) if self._records else np.zeros(0, _abi.ITER_RECORD_DTYPE)
+        return list(_DecisionLog(recs)) if self.config.log_decisions else []
+
     def _row_objects(self):
         """Trace-order row k -> its Request object (reference objects, built on first use)."""
         if getattr(self, "_rows", None) is None:

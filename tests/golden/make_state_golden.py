@@ -7,7 +7,8 @@ For each case the reference Engine runs with EngineConfig(iteration_limit=k) for
 several k; when it stops (SimulationAborted, engine.py:376-379) its `running` list
 (engine.py:205, execution order) and `waiting` queue (engine.py:160-176, 277-281)
 are the state after k iterations.  Recorded: running as (rel_id, req_id), waiting as
-(rel_id, pending req_ids' first and count, priority.hex()).
+(rel_id, pending req_ids' first and count, priority.hex()), the live relQueries (dict
+order), the ledgers (engine.py:52-61) and the decision log so far.
 """
 
 from __future__ import annotations
@@ -47,7 +48,11 @@ def snapshot(trace_kw, policy, cons, k):
             "kv_reserved": eng.kv_reserved,
             "running": [[r.rel_id, r.req_id] for r in eng.running],
             "waiting": [[w.relquery.rel_id, w.pending[0].req_id, len(w.pending), w.priority.hex()]
-                        for w in eng.waiting]}
+                        for w in eng.waiting],
+            "live": list(eng.live_relqueries),
+            "ledgers": [[k, v.arrival, v.first_prefill_start, v.last_prefill_end, v.last_decode_end]
+                        for k, v in eng.ledgers.items()],
+            "log": [[e.iteration, e.case, e.action] for e in eng.decision_log]}
 
 
 def main():

@@ -1,7 +1,8 @@
 """Engine state between steps equals relsim's (goldens: tests/golden/make_state_golden.py):
 after k iterations, `Engine.running` (engine.py:205, execution order) and `Engine.waiting`
 (engine.py:160-176, ordered by (priority, arrival, rel_id)) hold the same requests and
-relQuery entries, and the clock and kv reservation agree bit for bit."""
+relQuery entries, `live_relqueries`, `ledgers` and `decision_log` agree, and the clock and
+kv reservation agree bit for bit."""
 
 import gzip
 import json
@@ -35,5 +36,9 @@ def test_running_and_waiting_between_steps(name):
             assert [[r.rel_id, r.req_id] for r in eng.running] == snap["running"], snap["k"]
             assert [[w.relquery.rel_id, w.pending[0].req_id, len(w.pending), w.priority.hex()]
                     for w in eng.waiting] == snap["waiting"], snap["k"]
+            assert list(eng.live_relqueries) == snap["live"], snap["k"]
+            assert [[k, v.arrival, v.first_prefill_start, v.last_prefill_end, v.last_decode_end]
+                    for k, v in eng.ledgers.items()] == snap["ledgers"], snap["k"]
+            assert [[e.iteration, e.case, e.action] for e in eng.decision_log] == snap["log"], snap["k"]
     finally:
         eng.close()
