@@ -571,6 +571,37 @@ class Engine:
                 if sizes[i] == 0 or done_rows[i] < sizes[i]}
 
     @property
+    def next_arrival(self) -> float | None:
+        """relsim's ``Engine.next_arrival`` (engine.py:271-275): the arrival time of the next
+        relQuery not admitted yet, or None."""
+        c = self.trace.columns()
+        n_adm = int(self._status.admitted) if self._status is not None else 0
+        if n_adm >= c.num_relqueries:
+            return None
+        return float(c.arrival[np.lexsort((c.rel_id, c.arrival))[n_adm]])
+
+    @property
+    def kv_resident_tokens(self) -> int:
+        """relsim's ``Engine.kv_resident_tokens`` (engine.py:365-367): tok + generated over the
+        running requests."""
+        rows = self.running_rows
+        if not len(rows):
+            return 0
+        c = self.trace.columns()
+        gen, _, _, _ = self._native.read_requests(0, c.num_requests)
+        return int(c.tok[rows].sum() + gen[rows].sum())
+
+    @property
+    def dpu_wall(self) -> float:
+        """Device time of the priority updates so far (relsim's ``dpu_wall``, engine.py:381-386)."""
+        return self._phase_seconds(self._status, _DPU_PHASES) if self._status is not None else 0.0
+
+    @property
+    def aba_wall(self) -> float:
+        """Device time of the waiting order, candidates and decisions so far (relsim's ``aba_wall``)."""
+        return self._phase_seconds(self._status, _ABA_PHASES) if self._status is not None else 0.0
+
+    @property
     def decision_log(self) -> list:
         """relsim's ``Engine.decision_log`` (engine.py:209, 419-433): the entries of the iterations
         run so far."""

@@ -52,7 +52,8 @@ def snapshot(trace_kw, policy, cons, k):
             "live": list(eng.live_relqueries),
             "ledgers": [[k, v.arrival, v.first_prefill_start, v.last_prefill_end, v.last_decode_end]
                         for k, v in eng.ledgers.items()],
-            "log": [[e.iteration, e.case, e.action] for e in eng.decision_log]}
+            "log": [[e.iteration, e.case, e.action] for e in eng.decision_log],
+            "next_arrival": eng.next_arrival, "kv_resident_tokens": eng.kv_resident_tokens}
 
 
 def main():

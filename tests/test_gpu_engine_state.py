@@ -40,5 +40,7 @@ def test_running_and_waiting_between_steps(name):
             assert [[k, v.arrival, v.first_prefill_start, v.last_prefill_end, v.last_decode_end]
                     for k, v in eng.ledgers.items()] == snap["ledgers"], snap["k"]
             assert [[e.iteration, e.case, e.action] for e in eng.decision_log] == snap["log"], snap["k"]
+            assert eng.next_arrival == snap["next_arrival"], snap["k"]
+            assert eng.kv_resident_tokens == snap["kv_resident_tokens"], snap["k"]
     finally:
         eng.close()
