@@ -402,6 +402,58 @@ __device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shar
   return true;
 }
 
+// The prefill candidate's scan (arranger.py:80-112) over the head h's pending rows:
+// S.cand_tok / cand_out / cand_u (inclusive utok prefix) and S.first_bad, the first
+// row that breaks a constraint (S.first_bad must be 0x7FFFFFFF on entry); J = the rows
+// scanned at most, mh = B * resident chain blocks of h.  All threads of group G.
+template <bool kC, class G>
+__device__ __forceinline__ void cand_scan(const Params& P, const TraceDev& T, Shared& S, const int h, int& J,
+                                          int& mh) {
+  const Ctl& c = S.c;
+  const RqView& rq = S.rq;
+  const rs_config& cfg = P.cfg;
+  const int tid = threadIdx.x;
+  int base_row = 0, olh = 0;
+  J = 0;
+  mh = 0;
+  if (h >= 0) {
+    const int q = rq.q[h];
+    base_row = rq.off[h] + q;
+    const int pend = rq.off[h + 1] - base_row;
+    const long long room = cfg.max_num_seqs - c.n_run;
+    J = room <= 0 ? 0 : (int)(pend < room ? pend : room);
+    mh = (int)((kC ? 16 : cfg.block_size) * (long long)rq.m[h]);
+    olh = rq.ol[h];
+  }
+  const long long headroom = cfg.cap - c.kv;
+  int cu = 0, ck = 0;
+  for (int base = 0; base < J; base += G::kN) {
+    const int j = base + tid;
+    int v[2] = {0, 0};
+    if (j < J) {
+      const int t = T.tok[base_row + j];
+      S.cand_tok[j] = t;
+      S.cand_out[j] = T.out[base_row + j];
+      v[0] = t - mh;   // exact utok (match_uncached, refresh=False)
+      v[1] = t + olh;  // kv need
+    }
+    int tot[2];
+    group_scan32<G, 2>(v, S.s32, tot, tid >> 5);
+    bool bad = false;
+    if (j < J) {
+      const int U = cu + v[0], K = ck + v[1];
+      S.cand_u[j] = U;
+      bad = (j > 0 && U > cfg.max_num_batched_tokens) || K > headroom;
+    }
+    const unsigned m = __ballot_sync(kFull, bad);
+    if (m && (tid & 31) == 0) atomicMin(&S.first_bad, base + (tid & ~31) + __ffs(m) - 1);
+    cu += tot[0];
+    ck += tot[1];
+    G::sync();
+    if (S.first_bad < J) break;
+  }
+}
+
 // kC: the common configuration, fixed at compile time (a DPU policy, tau = inf,
 // no world-model noise, one shard, decision log on,
 // the default block size 16 and sample size 8):
@@ -687,48 +739,22 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
       S.first_bad = 0x7FFFFFFF;
     }
     phase_mark(c, 11);
-    // prefill candidate: leading run of the head's pending rows (arranger.py:80-112)
+    // prefill candidate: leading run of the head's pending rows (arranger.py:80-112),
+    // scanned here or -- after a decode -- already by group M while group D finished
+    // the previous update (cand_scan: nothing it reads changes in between)
     const int h = head_l;
-    int J = 0, base_row = 0, mh = 0, olh = 0;
-    if (h >= 0) {
-      const int q = rq.q[h];
-      base_row = rq.off[h] + q;
-      const int pend = rq.off[h + 1] - base_row;
-      const long long room = cfg.max_num_seqs - c.n_run;
-      J = room <= 0 ? 0 : (int)(pend < room ? pend : room);
-      mh = (int)((kC ? 16 : cfg.block_size) * (long long)rq.m[h]);
-      olh = rq.ol[h];
-    }
-    const long long headroom = cfg.cap - c.kv;
-    int cu = 0, ck = 0;
-    for (int base = 0; base < J; base += NT) {
-      const int j = base + tid;
-      int v[2] = {0, 0};
-      if (j < J) {
-        const int t = T.tok[base_row + j];
-        S.cand_tok[j] = t;
-        S.cand_out[j] = T.out[base_row + j];
-        v[0] = t - mh;   // exact utok (match_uncached, refresh=False)
-        v[1] = t + olh;  // kv need
-      }
-      int tot[2];
-      group_scan32<GC, 2>(v, S.s32, tot, tid >> 5);
-      bool bad = false;
-      if (j < J) {
-        const int U = cu + v[0], K = ck + v[1];
-        S.cand_u[j] = U;
-        bad = (j > 0 && U > cfg.max_num_batched_tokens) || K > headroom;
-      }
-      const unsigned m = __ballot_sync(kFull, bad);
-      if (m && (tid & 31) == 0) atomicMin(&S.first_bad, base + (tid & ~31) + __ffs(m) - 1);
-      cu += tot[0];
-      ck += tot[1];
-      GC::sync();
-      if (S.first_bad < J) break;
+    const bool pre = kC && S.pc.valid && h >= 0 && h == S.pc.head;  // group-uniform
+    int J, mh;
+    if (pre) {
+      J = S.pc.J;
+      mh = S.pc.mh;
+    } else {
+      cand_scan<kC, GC>(P, T, S, h, J, mh);
     }
     if (tid == 0) {
-      const int taken = S.first_bad < J ? S.first_bad : J;
-      const int loaded = ((S.first_bad < J ? S.first_bad : J - 1) / NT + 1) * NT;
+      const int fb = pre ? S.pc.first_bad : S.first_bad;
+      const int taken = fb < J ? fb : J;
+      const int loaded = ((fb < J ? fb : J - 1) / NT + 1) * NT;
       c.alg_bytes += 8LL * (J < loaded ? J : loaded);  // candidate tok + out
       S.taken = taken;
       S.cand_mh = mh;
@@ -772,6 +798,7 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
             S.taken, need_proj ? rq.ol[S.head] : 0, need_proj ? S.n_dist : 0, TermProj{S.dterm, (long long)S.max_ol},
             S.W, action, kase, mp, mmn, dp, dm, dt);
     S.max_ol = 0;  // for the next projection
+    S.pc.valid = 0;  // (read by every thread of phase D before its barrier)
     S.action = action;
     c.zptr = zptr_new;
     if (z_cache) {  // valid until an admission or a prefill of that relQuery
@@ -817,6 +844,23 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
     const bool go = execute<kC, GM, true>(P, T, S, action);  // group-uniform
     if (tid == 0) S.go_exec = go;
     exec_done_arrive();
+    if (go && action == RS_ACTION_DECODE && S.head >= 0) {
+      // a decode leaves the waiting queue, the head's rows and chain as they were and
+      // group D's update is the longer branch: scan the next prefill candidate now,
+      // for the (likely unchanged) head (used by phase D if it is still the head)
+      const int hp = S.head;
+      if (tid == 0) S.first_bad = 0x7FFFFFFF;
+      GM::sync();
+      int J, mh;
+      cand_scan<kC, GM>(P, T, S, hp, J, mh);
+      if (tid == 0) {
+        S.pc.head = hp;
+        S.pc.J = J;
+        S.pc.mh = mh;
+        S.pc.first_bad = S.first_bad;
+        S.pc.valid = 1;
+      }
+    }
     return go;
   } else {
     return execute<kC, GAll, false>(P, T, S, action);
@@ -849,6 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
     S.pf_head = -1;  // no previous head to prefetch for
     S.spec_ok = 0;   // the launch's first update runs in place (dpu_update)
     S.max_ol = 0;
+    S.pc.valid = 0;
   }
   __syncthreads();
   if (S.c.status == RS_RUNNING) {

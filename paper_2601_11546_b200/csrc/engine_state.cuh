@@ -214,6 +214,11 @@ struct Shared {
   int cand_out[kMaxRun];
   int cand_u[kMaxRun];     // inclusive utok prefix of the candidate rows
   int first_bad, cand_mh;
+  // a candidate scanned after a decode (engine.cu), in its own 32-byte block: phase D
+  // reads it while thread 0 writes the fields around (no vector load may straddle them)
+  struct alignas(32) PreCand {
+    int valid, head, J, mh, first_bad, pad[3];
+  } pc;
   // DPU batch
   int est_rank[kEstBatch], est_off[kEstBatch], est_q[kEstBatch], est_nunp[kEstBatch];
   int est_ol[kEstBatch], est_m[kEstBatch], est_doff[kEstBatch + 1];
