@@ -660,29 +660,41 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
   } else {
     // 1b. running-row summaries after the advance (decode: gen + 1, finished rows leave)
-    for (int j = threadIdx.x - (kMWarps + 1) * 32; j < c.n_run; j += (kDWarps - 1) * 32) {
-      int e = -1, rem = 0;
-      const int a = c.run_rank[j];
-      const int g = c.run_gen[j] + (dec ? 1 : 0);
-      if (!dec || g < c.run_out[j]) {  // a decode's finished rows leave (workload.py:134-136)
-        int lo = 0, hi = n_est;          // the list is sorted by rank
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (S.spec_rank[mid] <= a) lo = mid;
-          else hi = mid;
+    //     two rows per thread in one pass (224 threads, up to 448 rows): their loads and
+    //     searches overlap instead of a second round
+    constexpr int kSum = (kDWarps - 1) * 32;
+    const int t = threadIdx.x - (kMWarps + 1) * 32;
+    for (int base = 0; base < c.n_run; base += 2 * kSum) {  // warp-uniform
+      int e[2] = {-1, -1}, rem[2] = {0, 0};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = base + u * kSum + t;
+        if (j < c.n_run) {
+          const int a = c.run_rank[j];
+          const int g = c.run_gen[j] + (dec ? 1 : 0);
+          if (!dec || g < c.run_out[j]) {  // a decode's finished rows leave (workload.py:134-136)
+            int lo = 0, hi = n_est;          // the list is sorted by rank
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (S.spec_rank[mid] <= a) lo = mid;
+              else hi = mid;
+            }
+            e[u] = lo;
+            rem[u] = S.spec_ol[lo] - g;
+          }
         }
-        e = lo;
-        rem = S.spec_ol[e] - g;
       }
-      const unsigned act = __activemask();
-      const unsigned peers = __match_any_sync(act, e);
-      if (e >= 0) {
-        const unsigned sum = __reduce_add_sync(peers, (unsigned)rem);
-        const unsigned mx = __reduce_max_sync(peers, (unsigned)rem);
-        if (lane == __ffs(peers) - 1) {
-          atomicAdd(&S.spec_L[e], __popc(peers));
-          atomicAdd(&S.spec_rsum[e], (int)sum);
-          atomicMax(&S.spec_rmax[e], (int)mx);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const unsigned peers = __match_any_sync(kFull, e[u]);
+        if (e[u] >= 0) {
+          const unsigned sum = __reduce_add_sync(peers, (unsigned)rem[u]);
+          const unsigned mx = __reduce_max_sync(peers, (unsigned)rem[u]);
+          if (lane == __ffs(peers) - 1) {
+            atomicAdd(&S.spec_L[e[u]], __popc(peers));
+            atomicAdd(&S.spec_rsum[e[u]], (int)sum);
+            atomicMax(&S.spec_rmax[e[u]], (int)mx);
+          }
         }
       }
     }
