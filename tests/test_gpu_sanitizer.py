@@ -1,7 +1,7 @@
 """compute-sanitizer racecheck / memcheck / synccheck over short device runs (SURVEY 5:
 race detection): the general kernel (sp, finite tau, noise, a sharded pool) and the
 common-configuration kernel with its pipelined update.  Skipped when
-compute-sanitizer is not on PATH."""
+compute-sanitizer is not on PATH or the GPU pool refuses to run it."""
 
 import os
 import shutil
@@ -74,5 +74,8 @@ def test_sanitizer_clean(tool, tmp_path):
         args += ["--racecheck-report", "hazard"]
     r = subprocess.run(args + [sys.executable, str(script)], capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
+    if "ran" not in out and "closed on this pool" in out:
+        # the GPU pool's compute-sanitizer wrapper refuses to run (pool policy, not a finding)
+        pytest.skip("compute-sanitizer closed on this GPU pool: " + out.strip().splitlines()[0][:120])
     assert "ran" in out, out[-3000:]
     assert r.returncode == 0, out[-3000:]
