@@ -1421,33 +1421,11 @@ static int sort_pairs_dev(unsigned long long* k, int* v, long long n, cudaStream
     return RS_OK;
   }
   const long long tiles = (n + kSortTile - 1) / kSortTile;
-  unsigned long long* hist = nullptr;
+  unsigned long long* gh = nullptr;
   unsigned* th = nullptr;
-  RS_CUDA(b.get(&hist, 8 * 256));
+  RS_CUDA(b.get(&gh, 8 * 256));
   RS_CUDA(b.get(&th, 256 * tiles));
-  RS_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(unsigned long long), st));
-  sort_global_hist<<<(unsigned)std::min<long long>(tiles * 4, 148 * 4), kSortThreads, 0, st>>>(k, n, hist);
-  RS_CUDA(cudaGetLastError());
-  std::vector<unsigned long long> hh(8 * 256);
-  RS_CUDA(cudaMemcpyAsync(hh.data(), hist, hh.size() * 8, cudaMemcpyDeviceToHost, st));
-  RS_CUDA(cudaStreamSynchronize(st));
-  unsigned long long *sk = k, *dk = k1;
-  int *sv = v, *dv = v1;
-  for (int p = 0; p < 8; ++p) {
-    bool same = false;
-    for (int d = 0; d < 256; ++d) same = same || hh[p * 256 + d] == (unsigned long long)n;
-    if (same) continue;  // the identity pass
-    sort_tile_hist<<<(unsigned)tiles, kSortThreads, 0, st>>>(sk, n, 8 * p, th, (int)tiles);
-    sort_scan<<<1, kSortThreads, 0, st>>>(th, 256 * tiles);
-    sort_tile_scatter<<<(unsigned)tiles, kSortThreads, 0, st>>>(sk, sv, dk, dv, n, 8 * p, th, (int)tiles);
-    RS_CUDA(cudaGetLastError());
-    std::swap(sk, dk);
-    std::swap(sv, dv);
-  }
-  if (sk != k) {
-    RS_CUDA(cudaMemcpyAsync(k, sk, n * 8, cudaMemcpyDeviceToDevice, st));
-    RS_CUDA(cudaMemcpyAsync(v, sv, n * 4, cudaMemcpyDeviceToDevice, st));
-  }
+  RS_CUDA(sort_pairs_enqueue(k, v, k1, v1, gh, th, n, st));
   RS_CUDA(cudaStreamSynchronize(st));
   return RS_OK;
 }
@@ -1508,9 +1486,10 @@ static size_t arena_need(const rs_trace_view& v, const rs_config* cfg, long long
                       4 * R + rq_bytes((int)R) + 16 + (size_t)fifo_cap * sizeof(FifoEnt) +
                       (kJumpBits + 32) * sizeof(JumpEntry) + (size_t)lc * sizeof(rs_iter_record) + sizeof(Ctl) +
                       12 * (R + 1) + 8 + 24 * R /* static-order sort scratch */ +
+                      8 * 8 * 256 + 4 * 256 * (R / kSortTile + 1) /* ... its grid passes' histograms */ +
                       4 * (R + 1) /* first-sight segments */ +
                       16 * (R + N / (size_t)std::max<long long>(cfg->max_num_seqs, 1) + 1) /* ... their descriptors */ +
-                      45 * 256;
+                      47 * 256;
   return (need + 255) & ~(size_t)255;
 }
 
@@ -1846,13 +1825,18 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
   }
   pc.mark("relQuery table");
   // static-order sort scratch (keys, their ping-pong copies, values' ping-pong copy)
-  const bool zsort = R > 1 && R <= kSortOneCta && (dpu || cfg->policy == RS_POLICY_SP);
-  unsigned long long *zk0 = nullptr, *zk1 = nullptr;
+  const bool zsort = R > 1 && R <= 0x7FFFFFF0LL && (dpu || cfg->policy == RS_POLICY_SP);
+  unsigned long long *zk0 = nullptr, *zk1 = nullptr, *zgh = nullptr;
   int* zv1 = nullptr;
+  unsigned* zth = nullptr;
   if (zsort) {
     TRY(dalloc(h, &zk0, R));
     TRY(dalloc(h, &zk1, R));
     TRY(dalloc(h, &zv1, R));
+    if (R > kSortOneCta) {  // the grid passes' histograms
+      TRY(dalloc(h, &zgh, 8 * 256));
+      TRY(dalloc(h, &zth, 256 * ((R + kSortTile - 1) / kSortTile)));
+    }
   }
   d.fifo_cap = 1;  // >= capacity + kMaxRun + 2: batched pushes precede evictions
   while (d.fifo_cap < cfg->capacity_blocks + kMaxRun + 2) d.fifo_cap <<= 1;
@@ -1909,19 +1893,19 @@ static int build_trace(const rs_trace_view& v, const rs_config* cfg, const rs_co
       const int Ri = (int)R;
       auto sort = [=]() -> int {
         static_keys_kernel<<<(unsigned)std::min<long long>((Ri + 255) / 256, 148 * 8), 256>>>(src, Ri, zk0, dv.zl);
-        sort_pairs_one_cta<<<1, kSortThreads>>>(zk0, dv.zl, zk1, zv1, Ri);
-        const cudaError_t ke = cudaGetLastError();
+        cudaError_t ke = cudaGetLastError();
+        if (ke == cudaSuccess) {
+          if (Ri <= kSortOneCta) {
+            sort_pairs_one_cta<<<1, kSortThreads>>>(zk0, dv.zl, zk1, zv1, Ri);
+            ke = cudaGetLastError();
+          } else {
+            ke = sort_pairs_enqueue(zk0, dv.zl, zk1, zv1, zgh, zth, Ri, 0);
+          }
+        }
         return ke == cudaSuccess ? RS_OK : fail(RS_ECUDA, std::string("static order sort: ") + cudaGetErrorString(ke));
       };
       if (h.deferred) h.pending.push_back(sort);
       else if ((rc = sort())) return rc;
-    } else if (R > kSortOneCta && (dpu || cfg->policy == RS_POLICY_SP)) {  // the multi-CTA passes (synchronous)
-      DevBuf b;
-      unsigned long long* k = nullptr;
-      if (b.get(&k, R) != cudaSuccess) return fail(RS_ENOMEM, "static order keys");
-      static_keys_kernel<<<(unsigned)std::min<long long>((R + 255) / 256, 148 * 8), 256>>>(
-          dpu ? d.fsprio : dv.prio, (int)R, k, dv.zl);
-      if ((rc = sort_pairs_dev(k, dv.zl, R, 0))) return rc;
     }
     if (shard_world > 1) {
       // the full order on the host: a shard keeps the relQueries it owns (shard.cuh),

@@ -18,16 +18,20 @@
 // bits).  Each pass: per-tile digit histograms, an exclusive scan in
 // (digit, tile) order, and a stable scatter that ranks each 1024-key chunk with
 // __match_any_sync per warp plus a per-digit scan over the warps.  Small
-// inputs (<= kSortOneCta keys) run every pass inside one CTA, one launch.
+// inputs (<= kSortOneCta keys) run every pass inside one CTA, one launch;
+// larger ones run each pass as three grid launches over kSortTile-key tiles,
+// stream-ordered with no host round trip (sort_pairs_enqueue): the identity
+// passes are recognised on the device from the all-pass digit histogram.
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace rsd {
 
 constexpr int kSortThreads = 1024;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortOneCta = 1 << 16;  // one-CTA sort up to this many keys
-constexpr int kSortTile = 16 * kSortThreads;  // keys per CTA tile of the multi-CTA passes
+constexpr int kSortOneCta = 4096;  // one-CTA sort up to this many keys (its passes run serially on one SM)
+constexpr int kSortTile = 2 * kSortThreads;  // keys per CTA tile of the multi-CTA passes
 
 struct SortChunkSmem {
   unsigned wcnt[kSortWarps][256];  // per-warp digit counts -> per-warp digit offsets
@@ -40,12 +44,22 @@ __device__ __forceinline__ unsigned sort_digit(unsigned long long k, int shift) 
   return (unsigned)(k >> shift) & 0xFFu;
 }
 
+// One count per key of digit d (d >= 256: no key) into h, one shared-memory
+// atomic per distinct digit of the warp (all 32 lanes must call it).
+__device__ __forceinline__ void hist_add(unsigned* h, unsigned d) {
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+  if (d < 256u && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
+}
+
 // Histogram of digit `shift` over keys [lo, hi) into sm.hist (zeroed here).
 __device__ __forceinline__ void sort_hist(const unsigned long long* keys, long long lo, long long hi, int shift,
                                           SortChunkSmem& sm) {
   for (int b = threadIdx.x; b < 256; b += kSortThreads) sm.hist[b] = 0;
   __syncthreads();
-  for (long long i = lo + threadIdx.x; i < hi; i += kSortThreads) atomicAdd(&sm.hist[sort_digit(keys[i], shift)], 1u);
+  for (long long c0 = lo; c0 < hi; c0 += kSortThreads) {  // warp-uniform trip count
+    const long long i = c0 + threadIdx.x;
+    hist_add(sm.hist, i < hi ? sort_digit(keys[i], shift) : 256u + (threadIdx.x & 31));
+  }
   __syncthreads();
 }
 
@@ -170,18 +184,27 @@ __global__ void __launch_bounds__(kSortThreads) sort_global_hist(const unsigned 
   __shared__ unsigned h[8][256];
   for (int b = threadIdx.x; b < 8 * 256; b += kSortThreads) (&h[0][0])[b] = 0;
   __syncthreads();
-  for (long long i = (long long)blockIdx.x * kSortThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kSortThreads) {
-    const unsigned long long k = keys[i];
+  for (long long c0 = (long long)blockIdx.x * kSortThreads; c0 < n; c0 += (long long)gridDim.x * kSortThreads) {
+    const long long i = c0 + threadIdx.x;  // warp-uniform trip count
+    const unsigned long long k = i < n ? keys[i] : 0ULL;
 #pragma unroll
-    for (int p = 0; p < 8; ++p) atomicAdd(&h[p][sort_digit(k, 8 * p)], 1u);
+    for (int p = 0; p < 8; ++p) hist_add(h[p], i < n ? sort_digit(k, 8 * p) : 256u + (threadIdx.x & 31));
   }
   __syncthreads();
   for (int b = threadIdx.x; b < 8 * 256; b += kSortThreads)
     if ((&h[0][0])[b]) atomicAdd(&hist[b], (unsigned long long)(&h[0][0])[b]);
 }
 
+// Pass `shift` is the identity when every key has the same digit there: the
+// count of any one key's digit (keys[0]'s) is n.  gh = sort_global_hist's counts.
+__device__ __forceinline__ bool sort_identity(const unsigned long long* keys, long long n, int shift,
+                                              const unsigned long long* gh) {
+  return gh[(shift >> 3) * 256 + sort_digit(keys[0], shift)] == (unsigned long long)n;
+}
+
 __global__ void __launch_bounds__(kSortThreads) sort_tile_hist(const unsigned long long* keys, long long n, int shift,
-                                                               unsigned* th, int n_tiles) {
+                                                               unsigned* th, int n_tiles, const unsigned long long* gh) {
+  if (gh && sort_identity(keys, n, shift, gh)) return;
   __shared__ SortChunkSmem sm;
   const long long lo = (long long)blockIdx.x * kSortTile;
   const long long hi = lo + kSortTile < n ? lo + kSortTile : n;
@@ -189,7 +212,9 @@ __global__ void __launch_bounds__(kSortThreads) sort_tile_hist(const unsigned lo
   for (int b = threadIdx.x; b < 256; b += kSortThreads) th[(long long)b * n_tiles + blockIdx.x] = sm.hist[b];
 }
 
-__global__ void __launch_bounds__(kSortThreads) sort_scan(unsigned* th, long long m) {
+__global__ void __launch_bounds__(kSortThreads) sort_scan(unsigned* th, long long m, const unsigned long long* keys,
+                                                          long long n, int shift, const unsigned long long* gh) {
+  if (gh && sort_identity(keys, n, shift, gh)) return;
   __shared__ unsigned wsum[kSortWarps];
   __shared__ unsigned carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -221,13 +246,46 @@ __global__ void __launch_bounds__(kSortThreads) sort_scan(unsigned* th, long lon
 
 __global__ void __launch_bounds__(kSortThreads) sort_tile_scatter(const unsigned long long* sk, const int* sv,
                                                                   unsigned long long* dk, int* dv, long long n,
-                                                                  int shift, const unsigned* th, int n_tiles) {
+                                                                  int shift, const unsigned* th, int n_tiles,
+                                                                  const unsigned long long* gh) {
   __shared__ SortChunkSmem sm;
   const long long lo = (long long)blockIdx.x * kSortTile;
   const long long hi = lo + kSortTile < n ? lo + kSortTile : n;
+  if (gh && sort_identity(sk, n, shift, gh)) {  // the identity pass: the tile as it is (keeps the ping-pong fixed)
+    for (long long i = lo + threadIdx.x; i < hi; i += kSortThreads) {
+      dk[i] = sk[i];
+      dv[i] = sv[i];
+    }
+    return;
+  }
   for (int b = threadIdx.x; b < 256; b += kSortThreads) sm.base[b] = th[(long long)b * n_tiles + blockIdx.x];
   __syncthreads();
   sort_scatter(sk, sv, dk, dv, lo, hi, shift, sm);
+}
+
+// The grid passes, enqueued on `st` with no host round trip: all eight digits
+// run (identity passes copy), so the sorted pairs end in (k, v).  Scratch:
+// (k1, v1) n pairs, gh 8 * 256 counts, th 256 * ceil(n / kSortTile) counts.
+inline cudaError_t sort_pairs_enqueue(unsigned long long* k, int* v, unsigned long long* k1, int* v1,
+                                      unsigned long long* gh, unsigned* th, long long n, cudaStream_t st) {
+  const long long tiles = (n + kSortTile - 1) / kSortTile;
+  cudaError_t e = cudaMemsetAsync(gh, 0, 8 * 256 * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  sort_global_hist<<<(unsigned)(tiles < 148 ? tiles : 148), kSortThreads, 0, st>>>(k, n, gh);
+  unsigned long long *sk = k, *dk = k1;
+  int *sv = v, *dv = v1;
+  for (int p = 0; p < 8; ++p) {
+    sort_tile_hist<<<(unsigned)tiles, kSortThreads, 0, st>>>(sk, n, 8 * p, th, (int)tiles, gh);
+    sort_scan<<<1, kSortThreads, 0, st>>>(th, 256 * tiles, sk, n, 8 * p, gh);
+    sort_tile_scatter<<<(unsigned)tiles, kSortThreads, 0, st>>>(sk, sv, dk, dv, n, 8 * p, th, (int)tiles, gh);
+    unsigned long long* tk = sk;
+    sk = dk;
+    dk = tk;
+    int* tv = sv;
+    sv = dv;
+    dv = tv;
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace rsd

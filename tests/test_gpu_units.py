@@ -92,7 +92,7 @@ def test_pem_reference_tests():
     assert pem([RemainderItem(None, 80, 4, False)] * 5, c, model) <= full
 
 
-@pytest.mark.parametrize("n", [0, 1, 2, 1000, 65536, 65537, 300_000])
+@pytest.mark.parametrize("n", [0, 1, 2, 1000, 4096, 4097, 40_000, 65537, 300_000])
 def test_radix_sort_is_a_stable_sort(n):
     """North-star kernel 2 (rs_sort_pairs): equals numpy's stable argsort, duplicates
     keeping their input order; keys built like the engine's (okey of priorities of
@@ -106,6 +106,17 @@ def test_radix_sort_is_a_stable_sort(n):
     ko, vo = _native.sort_pairs(keys, vals)
     order = np.argsort(keys, kind="stable")
     assert np.array_equal(vo, vals[order]) and np.array_equal(ko, keys[order])
+
+
+@pytest.mark.parametrize("n", [3000, 50_000])
+def test_radix_sort_equal_and_sorted_keys(n):
+    """Every pass the identity (all keys equal), and an already sorted input with ties: the
+    grid passes recognise identity passes on the device (radix_sort.cuh)."""
+    vals = np.arange(n, dtype=np.int32)
+    for keys in (np.full(n, 0x3FF0000000000000, dtype=np.uint64),
+                 np.sort(np.random.default_rng(n).integers(0, 1000, n).astype(np.uint64))):
+        ko, vo = _native.sort_pairs(keys, vals)
+        assert np.array_equal(ko, keys) and np.array_equal(vo, vals)
 
 
 def test_priority_keys_order_numbers():

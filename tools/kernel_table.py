@@ -6,7 +6,7 @@
           --clock-control none --csv --log-file gpurun_out/kernels_$w.csv python tools/kernel_table.py run $w
     done
     # here: the table
-    python tools/kernel_table.py table profiles/r2/kernels.md gpurun_out/kernels_{c2,c5,c3p}.csv
+    python tools/kernel_table.py table profiles/r2/kernels.md profiles/r2/kernels/kernels_{c2,c5,c3p}.csv
 
 `run` drives each kernel family once on its natural workload:
   * config 2 (10^6 requests): engine creation (row checks, static order, first sight) + 2 launches of
@@ -93,7 +93,9 @@ def table(out_md: str, *csv_paths: str):
              "frac of %.0f GB/s |" % peak, "|---|---|---|---|---|---|---|---|"]
     summary = []
     for (w, name), d in sorted(per.items(), key=lambda kv: (kv[0][0], -kv[1]["gpu__time_duration.sum"])):
-        n = len(seen[name])
+        n = len(seen[(w, name)])
+        if not d["gpu__time_duration.sum"]:
+            continue
         t = d["gpu__time_duration.sum"] / n
         dram = (d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]) / n
         l2 = d["lts__t_bytes.sum"] / n
@@ -102,7 +104,17 @@ def table(out_md: str, *csv_paths: str):
         lines.append(f"| {w} | `{short}` | {n} | {t * 1e6:.1f} | {dram:,.0f} | {l2:,.0f} | {gbs:.0f} | {gbs / peak:.3f} |")
         summary.append(dict(workload=w, kernel=short, launches=n, us=t * 1e6, dram_bytes=dram, l2_bytes=l2, gbs=gbs,
                             frac=gbs / peak))
-    Path(out_md).write_text("\n".join(lines) + "\n")
+    head = ["# Every kernel of the repository: ncu duration and DRAM traffic per launch", "",
+            "Generated by `tools/kernel_table.py` (its docstring has the commands) from ncu's per-launch metrics "
+            "(`gpu__time_duration.sum`, `dram__bytes_read.sum + dram__bytes_write.sum`, `lts__t_bytes.sum`; "
+            "cold-cache, serialised launches, `--clock-control none`); raw CSVs in `kernels/`.  DRAM GB/s = DRAM "
+            "bytes / duration, against MEASURED_PEAKS.json's copy bandwidth.  `engine_kernel` is one persistent "
+            "CTA running hundreds of dependent scheduler iterations per launch (latency-bound, DESIGN.md 5: "
+            "its yardstick is cycles per iteration); the creation kernels (`validate_rows_kernel`, "
+            "`first_sight_seg_kernel`, `first_sight_sum_kernel`) stream the trace columns once; the radix-sort "
+            "kernels order the static waiting queue at creation and, in parity mode, every recorded iteration's "
+            "full waiting queue.", ""]
+    Path(out_md).write_text("\n".join(head + lines) + "\n")
     Path(out_md).with_suffix(".json").write_text(json.dumps(dict(peak_gbs=peak, kernels=summary), indent=1))
     print("\n".join(lines))
 
