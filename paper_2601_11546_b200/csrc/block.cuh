@@ -28,6 +28,31 @@ __device__ __forceinline__ int opaque_lane() {
   return (int)l;
 }
 
+// Stable in-place compaction of list[0, n) to the entries x with keep(x), by
+// one whole warp, 32 entries per round; returns the new length (every lane).
+// Each round's entries are all read (the ballot) before any is written, and
+// writes land below the round's end, so later rounds read unmoved entries.
+template <class F>
+__device__ __forceinline__ int warp_compact(int* list, const int n, F keep) {
+  const int lane = threadIdx.x & 31;
+  int w = 0;
+#pragma unroll 1
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    int x = 0;
+    bool k = false;
+    if (i < n) {
+      x = list[i];
+      k = keep(x);
+    }
+    const unsigned m = __ballot_sync(kFull, k);
+    if (k) list[w + __popc(m & ((1u << lane) - 1u))] = x;
+    w += __popc(m);
+  }
+  __syncwarp();
+  return w;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
   const int lane = threadIdx.x & 31;

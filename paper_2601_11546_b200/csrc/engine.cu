@@ -346,6 +346,19 @@ __device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shar
       }
     }
     G::sync();
+    if (opaque_warp() == 0) {
+      // warp 0: the distinct running relQueries without running rows leave rrq, retired
+      // relQueries the re-estimate list (stable compactions, 32 entries per round: the
+      // relQuery table may sit in HBM, where a serial loop pays a load latency per entry)
+      if (S.rrq_dirty) {
+        const int w = warp_compact(c.rrq, c.n_rrq, [&](int a) { return rq.nrun[a] > 0; });
+        if (opaque_lane() == 0) c.n_rrq = w;
+      }
+      if (S.act_dirty && (kC || P.use_dpu)) {
+        const int w = warp_compact(c.act, c.n_act, [&](int a) { return rq.ndone[a] < rq.off[a + 1] - rq.off[a]; });
+        if (opaque_lane() == 0) c.n_act = w;
+      }
+    }
     if (tid == 0) {
       c.alg_bytes += 8LL * (n - cbase);  // generated + completion iteration of finished rows
       c.n_run = cbase;
@@ -353,20 +366,6 @@ __device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shar
       c.clock = clk;
       c.n_batch++;
       if (kC || (cfg.log_decisions && T.log_cap > 0)) T.log[c.n_log & (T.log_cap - 1)].batch_n = n;
-      if (S.rrq_dirty) {
-        int w = 0;
-        for (int i = 0; i < c.n_rrq; ++i)
-          if (rq.nrun[c.rrq[i]] > 0) c.rrq[w++] = c.rrq[i];
-        c.n_rrq = w;
-      }
-      if (S.act_dirty && (kC || P.use_dpu)) {  // drop retired relQueries from the re-estimate list
-        int w = 0;
-        for (int i = 0; i < c.n_act; ++i) {
-          const int a = c.act[i];
-          if (rq.ndone[a] < rq.off[a + 1] - rq.off[a]) c.act[w++] = a;
-        }
-        c.n_act = w;
-      }
     }
   } else {  // idle (engine.py:439-447)
     if constexpr (kHand) handoff_wait();
