@@ -216,6 +216,11 @@ __device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shar
     const int n = S.taken;
     const int n_run0 = c.n_run;
     const int ol = rq.ol[h];
+    // read before the cache advance (nothing in this iteration changes them before thread 0's
+    // bookkeeping): their latency -- HBM when the relQuery table does not fit in shared
+    // memory -- overlaps the advance instead of thread 0's serial section
+    const int size_h = rq.off[h + 1] - rq.off[h];
+    const int nrun_h = rq.nrun[h];
     long long ut = 0;
     const bool fast = prefill_fast<kC, G, kHand>(P, T, S, h, n, S.cand_tok, ut);
     if (kHand && !fast) handoff_wait();  // the exact per-row path changes rq.m too
@@ -240,9 +245,9 @@ __device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shar
         c.n_run = n_run0 + n;
         rq.q[h] = q + n;
         if (h == c.zh_idx) c.zh_valid = 0;  // the cached static-order head may have left the order
-        if (q + n == rq.off[h + 1] - rq.off[h]) c.n_wait--;  // no pending rows left: leaves waiting
-        if (rq.nrun[h] == 0) c.rrq[c.n_rrq++] = h;
-        rq.nrun[h] += n;
+        if (q + n == size_h) c.n_wait--;  // no pending rows left: leaves waiting
+        if (nrun_h == 0) c.rrq[c.n_rrq++] = h;
+        rq.nrun[h] = nrun_h + n;
         if (q == 0 && (kC || P.use_dpu)) {  // becomes partially prefilled: join the re-estimate list
           int pos = c.n_act;
           if (pos >= kMaxAct) {
@@ -311,8 +316,10 @@ __device__ __forceinline__ bool execute(const Params& P, const TraceDev& T, Shar
           T.gen[r] = g;
           T.comp[r] = (int)c.iteration;
           kv_free += nkv[s];
-          if (atomicSub(&rq.nrun[a], 1) == 1) S.rrq_dirty = 1;
-          if (atomicAdd(&rq.ndone[a], 1) + 1 == rq.off[a + 1] - rq.off[a]) {
+          const int nrun_old = atomicSub(&rq.nrun[a], 1);  // both in flight at once
+          const int ndone_old = atomicAdd(&rq.ndone[a], 1);
+          if (nrun_old == 1) S.rrq_dirty = 1;
+          if (ndone_old + 1 == rq.off[a + 1] - rq.off[a]) {
             T.lde[a] = clk;  // relQuery retired (engine.py:360-362)
             atomicSub(&c.live, 1);
             S.act_dirty = 1;
@@ -2188,11 +2195,26 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && cfg->log_decisions &&
               cfg->block_size == 16 && cfg->sample_size == 8;
   for (auto& h : e->traces) e->common = e->common && h.dev.log_cap > 0;
-  cudaError_t ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  if (ce == cudaSuccess)
-    ce = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  if (ce == cudaSuccess)
-    ce = cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  // the kernels' dynamic shared-memory limit only grows (engines with different needs may coexist);
+  // the L1/shared carve-out is left to the driver, which sizes it by each launch's request
+  static std::mutex attr_mu;
+  static size_t smem_limit = 0;
+  cudaError_t ce = cudaSuccess;
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    const size_t lim = std::max(smem_limit, e->smem);
+    ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    if (ce == cudaSuccess)
+      ce = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    if (ce == cudaSuccess)
+      ce = cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+#ifdef RS_CARVEOUT  // experiment: ask for the smallest carve-out that holds this engine's shared memory
+    const int pct = (int)std::min<size_t>(100, (e->smem + 1024) * 100 / (228 * 1024) + 1);
+    if (ce == cudaSuccess)
+      ce = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+#endif
+    if (ce == cudaSuccess) smem_limit = lim;
+  }
   if (ce != cudaSuccess) return bail(fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
   pc.mark("kernel attributes");
   *out = e;

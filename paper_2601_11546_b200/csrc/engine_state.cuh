@@ -31,7 +31,10 @@ constexpr int kMaxCC = 256;     // tail-less resident chains
 constexpr int kWin = 768;       // FIFO window of the batched prefill eviction
 constexpr int kEstBatch = 128;  // relQueries re-estimated per DPU batch
 constexpr int kDrawBuf = 4096;  // numpy next32 draws staged per DPU batch
-constexpr int kItemBuf = 2048;  // PEM items staged per segment-parallel batch
+#ifndef RS_ITEM_BUF
+#define RS_ITEM_BUF 1536  // keeps Shared below the 132 KB carve-out (a larger L1 for traces whose relQuery table is in HBM)
+#endif
+constexpr int kItemBuf = RS_ITEM_BUF;  // PEM items staged per segment-parallel batch
 constexpr int kPhases = 24;
 constexpr int kSmallEst = 32;   // DPU fast path: at most this many re-estimated relQueries
 constexpr int kSmallMns = 256;  // ... and max_num_seqs at most this
