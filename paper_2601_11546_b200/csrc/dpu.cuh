@@ -488,6 +488,7 @@ __device__ int dpu_small(const Params& P, const TraceDev& T, Shared& S, const Pe
 // fast path's shape (<= kSmallEst relQueries, <= kMaxJobs PEM segments, no
 // Lemire rejection) is speculated; otherwise the next iteration runs
 // dpu_update in place.
+template <bool kPart>
 __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const int action, const int h, const int nh,
                          const bool allowed) {
   Ctl& c = S.c;
@@ -497,7 +498,11 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
   dphase_mark(c, -1);
   const int n_act = c.n_act;
   const bool join = pf && rq.q[h] == 0;  // h's first prefill: it joins the list
-  const int n_est = n_act + (join ? 1 : 0);
+  // kPart, more than kSmallEst entries: the first kSmallEst are computed here and
+  // the next iteration's phase B estimates the rest in place, continuing the
+  // generator (else such an update runs wholly in place)
+  const int n_full = n_act + (join ? 1 : 0);
+  const int n_est = kPart && n_full > kSmallEst ? kSmallEst : n_full;
 #ifdef RS_NO_SPEC  // experiment: the pipelined update disabled (every update runs in place)
   const bool no_spec = true;
 #else
@@ -507,6 +512,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     if (threadIdx.x == kMWarps * 32) {
       S.spec_valid = !no_spec && n_est == 0 && allowed;  // nothing to re-estimate: trivially done
       S.spec_n = 0;
+      if constexpr (kPart) S.spec_part = 0;
       S.spec_rng = c.rng;
       S.spec_alg = 0;
     }
@@ -562,6 +568,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
     }
     if (lane == 0) {
       S.spec_n = n_est;
+      if constexpr (kPart) S.spec_part = n_full > n_est;
       S.spec_valid = 1;
     }
   }
@@ -679,8 +686,10 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
               if (S.spec_rank[mid] <= a) lo = mid;
               else hi = mid;
             }
-            e[u] = lo;
-            rem[u] = S.spec_ol[lo] - g;
+            if (!kPart || S.spec_rank[lo] == a) {  // (a partial list holds only the first kSmallEst)
+              e[u] = lo;
+              rem[u] = S.spec_ol[lo] - g;
+            }
           }
         }
       }
@@ -854,6 +863,7 @@ __device__ void dpu_spec(const Params& P, const TraceDev& T, Shared& S, const in
 // iteration's if every chain length it assumed is the advance's; retiring
 // relQueries (no unprefilled and no running row left) are not written.  The
 // entries kept must be exactly the advance's act list.
+template <bool kPart>
 __device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -873,7 +883,12 @@ __device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
                    c.act[__popc(__ballot_sync(__activemask(), keep) & ((1u << lane) - 1u))] != a);
   }
   const unsigned km = __ballot_sync(kFull, keep);
-  ok = ok && !__any_sync(kFull, bad) && __popc(km) == c.n_act;
+  const int nk = __popc(km);
+  // complete: the kept entries are the whole list; partial (the first kSmallEst of a
+  // longer list): they are its first nk entries and the next entry lies past them
+  const bool tail_ok = kPart && S.spec_part ? nk <= c.n_act && (nk == c.n_act || c.act[nk] > S.spec_rank[n - 1])
+                                            : nk == c.n_act;
+  ok = ok && !__any_sync(kFull, bad) && tail_ok;
   if (ok && keep) rq.prio[a] = S.spec_val[lane];
   if (lane == 0) {
     if (ok) {
@@ -881,8 +896,10 @@ __device__ __forceinline__ void spec_commit(Shared& S, const TraceDev& T) {
       c.alg_bytes += S.spec_alg;
     }
     S.spec_ok = ok;
+    if constexpr (kPart) S.spec_e0 = ok && S.spec_part ? nk : -1;  // where phase B's continuation starts
   }
 }
+
 
 // First sight of this iteration's arrivals [new_lo, new_hi): none of their
 // rows is prefilled and their shared chain is not resident (no row of theirs
@@ -1264,8 +1281,10 @@ __device__ void dpu_batched(const Params& P, const TraceDev& T, Shared& S, const
   }
 }
 
-template <bool kFast, bool kC>
-__device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
+// e_start: the first entry of the re-estimate list to estimate (> 0 after a
+// partial speculative update, which covered the entries before it).
+template <bool kFast, bool kC, bool kPart = false>
+__device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S, const int e_start = 0) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
   const rs_config& cfg = P.cfg;
@@ -1281,7 +1300,7 @@ __device__ void dpu_update(const Params& P, const TraceDev& T, Shared& S) {
   if constexpr (kFast) {
     // partially prefilled relQueries (in rank order), then the arrivals
     const int n_act = c.n_act;
-    for (int e0 = 0; e0 < n_act;) {
+    for (int e0 = kPart ? e_start : 0; e0 < n_act;) {
       e0 += dpu_small<kC>(P, T, S, pm, e0, n_act);
       __syncthreads();
     }

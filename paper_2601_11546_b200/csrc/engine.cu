@@ -464,7 +464,7 @@ __device__ __forceinline__ void cand_scan(const Params& P, const TraceDev& T, Sh
 // no world-model noise, one shard, decision log on,
 // the default block size 16 and sample size 8):
 // the checks for everything else leave the iteration's instruction stream.
-template <bool kFast, bool kC>
+template <bool kFast, bool kC, bool kPart>
 __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const bool last) {
   Ctl& c = S.c;
   const RqView& rq = S.rq;
@@ -528,8 +528,11 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   // ---- B: priorities.  fcfs: 0.0; sp: static_relquery_prio, both set at
   // admission (engine.py:255-267, preloaded into prio); relserve*: the DPU.
   if constexpr (kC) {
-    if (!S.spec_ok) {  // the launch's first iteration, or the speculative update was not usable
-      dpu_update<kFast, kC>(P, T, S);
+    // the launch's first iteration, the speculative update was not usable, or (kPart) it
+    // covered a prefix of the list only
+    if (!S.spec_ok || (kPart && S.spec_e0 >= 0)) {
+      if constexpr (kPart) dpu_update<kFast, kC, true>(P, T, S, S.spec_ok ? S.spec_e0 : 0);
+      else dpu_update<kFast, kC>(P, T, S);
     } else {  // the re-estimates were computed during the previous advance: only the arrivals remain
       if (S.new_hi > S.new_lo) first_sight(P, T, S, S.new_lo, S.new_hi);
       if (tid == 0) S.n_est = c.n_act + (S.new_hi - S.new_lo);
@@ -567,9 +570,9 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
         }
       }
       if ((threadIdx.x & 31) == 0 && opaque_warp() == kMWarps) S.spec_action = action;
-      dpu_spec(P, T, S, action, h, nh, allowed);
+      dpu_spec<kPart>(P, T, S, action, h, nh, allowed);
       exec_done_wait();
-      if (opaque_warp() == kMWarps) spec_commit(S, T);
+      if (opaque_warp() == kMWarps) spec_commit<kPart>(S, T);
       return S.go_exec;
     }
   }
@@ -879,7 +882,9 @@ __device__ __forceinline__ void copy16(void* dst, const void* src, size_t bytes)
   for (size_t i = threadIdx.x; i < bytes / 16; i += kThreads) d[i] = s[i];
 }
 
-template <bool kFast, bool kC>
+// kPart (common configuration, a relQuery table in HBM: configs 3 and 5): the
+// pipelined update may cover the first kSmallEst entries of a longer list
+template <bool kFast, bool kC, bool kPart = false>
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ TraceDev Tsm;  // the trace's pointers, read on every access
@@ -905,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(Params P) {
   if (S.c.status == RS_RUNNING) {
     if (threadIdx.x == 0) S.c.phase[kPhases - 1] = clock64();
     for (long long it = 0; it < P.max_iters; ++it)
-      if (!iterate<kFast, kC>(P, T, S, it + 1 == P.max_iters)) break;
+      if (!iterate<kFast, kC, kPart>(P, T, S, it + 1 == P.max_iters)) break;
   }
   __syncthreads();
   // running rows' generated counts back to HBM (finished rows were written at completion)
@@ -1446,6 +1451,7 @@ struct rs_engine {
   bool connected = true;                 // one-shard engines: peers' mailboxes known (rs_engine_connect)
   bool fast = true;  // every trace qualifies for engine_kernel<true, *>
   bool common = false;  // ... and the configuration is the common one (engine_kernel<true, true>)
+  bool part = false;    // ... with a relQuery table in HBM (engine_kernel<true, true, true>)
   Params params{};
   std::vector<HostTrace> traces;
   TraceDev* d_traces = nullptr;
@@ -2195,6 +2201,8 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
   e->common = e->fast && p.use_dpu && std::isinf(cfg->tau) && !(cfg->noise_sigma > 0) && cfg->log_decisions &&
               cfg->block_size == 16 && cfg->sample_size == 8;
   for (auto& h : e->traces) e->common = e->common && h.dev.log_cap > 0;
+  e->part = false;  // a relQuery table in HBM (large traces: long re-estimate lists are common)
+  for (auto& h : e->traces) e->part = e->part || !h.dev.rq_in_smem;
   // the kernels' dynamic shared-memory limit only grows (engines with different needs may coexist);
   // the L1/shared carve-out is left to the driver, which sizes it by each launch's request
   static std::mutex attr_mu;
@@ -2206,6 +2214,8 @@ static int create_impl(const rs_trace_view* traces, int32_t n_traces, const rs_c
     ce = cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
     if (ce == cudaSuccess)
       ce = cudaFuncSetAttribute(engine_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    if (ce == cudaSuccess)
+      ce = cudaFuncSetAttribute(engine_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
     if (ce == cudaSuccess)
       ce = cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
 #ifdef RS_CARVEOUT  // experiment: ask for the smallest carve-out that holds this engine's shared memory
@@ -2315,7 +2325,9 @@ int rs_engine_step(rs_engine* e, int64_t max_iters, void* stream) {
   if (e->ready) RS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, e->ready, 0));  // creation's uploads / kernels
   Params p = e->params;
   p.max_iters = max_iters;
-  if (e->common)
+  if (e->common && e->part)
+    engine_kernel<true, true, true><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
+  else if (e->common)
     engine_kernel<true, true><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);
   else if (e->fast)
     engine_kernel<true, false><<<(unsigned)e->traces.size(), kThreads, e->smem, (cudaStream_t)stream>>>(p);

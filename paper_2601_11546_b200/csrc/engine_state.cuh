@@ -283,6 +283,9 @@ struct Shared {
       } win;
     };
   };
+  // kPart (engine_kernel<true, true, true>) only; last, so the other fields keep their offsets
+  int spec_part;  // the speculative list is the first kSmallEst entries of a longer one
+  int spec_e0;    // after a partial commit: the first entry phase B estimates in place (else -1)
   // relQuery table follows (dynamic shared memory) when rq_in_smem
 };
 

@@ -45,6 +45,23 @@ def _common_case(i):
     return tc, cons, kw, policy, model, seed, 1
 
 
+def _long_list_case(i):
+    """The common configuration on traces whose relQuery table lives in HBM (more than
+    ~1,300 relQueries) and whose re-estimate lists often exceed 32 entries: the pipelined
+    update covers the first 32 and phase B estimates the rest in place (engine_kernel's
+    kPart instantiation)."""
+    r = np.random.default_rng(7000 + i)
+    tc = dict(num_relqueries=int(r.choice([1500, 2200])), size_range=(1, int(r.choice([12, 40, 90]))),
+              rate=float(r.choice([2e3, 1e6])), seed=int(r.integers(0, 10_000)), mean_input_len=120)
+    policy = ("relserve", "relserve-pp", "relserve-dp")[i % 3]
+    return tc, (200_000, 256, 8192), dict(iteration_limit=1500), policy, MODELS[i % 3], int(r.integers(0, 100)), 1
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_long_reestimate_lists_equal_oracle(i, oracle_mod):
+    _sweep_case(_long_list_case(i), oracle_mod, min_reestimated=33)
+
+
 @pytest.mark.parametrize("i", range(120))
 def test_random_sweep_device_equals_oracle(i, oracle_mod):
     _sweep_case(_case(i), oracle_mod)
@@ -55,14 +72,14 @@ def test_random_sweep_common_kernel_equals_oracle(i, oracle_mod):
     _sweep_case(_common_case(i), oracle_mod)
 
 
-def _sweep_case(case, oracle_mod):
+def _sweep_case(case, oracle_mod, min_reestimated=0):
     from paper_2601_11546_b200 import EngineConfig, SchedulerConstraints, TraceConfig, generate_trace, world_preset
     from paper_2601_11546_b200.engine import Engine
     from paper_2601_11546_b200.priority import InfeasibleRequestError
 
     tc, cons, kw, policy, model, seed, shards = case
     trace = generate_trace(TraceConfig(**tc))
-    cfg = EngineConfig(constraints=SchedulerConstraints(*cons), iteration_limit=20_000, **kw)
+    cfg = EngineConfig(constraints=SchedulerConstraints(*cons), **{"iteration_limit": 20_000, **kw})
     w = world_preset(model)
     O = oracle_mod
     ref = O.run(trace, policy, w, cfg, None, seed, record=O.OR_REC_DPU | O.OR_REC_WAITING | O.OR_REC_RNG)
@@ -89,6 +106,8 @@ def _sweep_case(case, oracle_mod):
         a, b = res.records[k], ref.log[k]
         assert np.array_equal(a, b, equal_nan=a.dtype.kind == "f"), k
     assert np.array_equal(res.completion_iteration, ref.completion_iter)
+    if min_reestimated:  # the case exercises what it is meant to
+        assert res.records["n_reestimated"][1:].max() >= min_reestimated
     assert (res.cache_hit_tokens, res.cache_miss_tokens) == (ref.cache_hit_tokens, ref.cache_miss_tokens)
     n = len(ref.log)
     rel = trace.columns().rel_id
