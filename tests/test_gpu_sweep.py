@@ -54,10 +54,11 @@ def _long_list_case(i):
     tc = dict(num_relqueries=int(r.choice([1500, 2200])), size_range=(1, int(r.choice([12, 40, 90]))),
               rate=float(r.choice([2e3, 1e6])), seed=int(r.integers(0, 10_000)), mean_input_len=120)
     policy = ("relserve", "relserve-pp", "relserve-dp")[i % 3]
-    return tc, (200_000, 256, 8192), dict(iteration_limit=1500), policy, MODELS[i % 3], int(r.integers(0, 100)), 1
+    shards = 3 if i % 4 == 3 else 1  # the sharded pool runs the same instantiation
+    return tc, (200_000, 256, 8192), dict(iteration_limit=1500), policy, MODELS[i % 3], int(r.integers(0, 100)), shards
 
 
-@pytest.mark.parametrize("i", range(6))
+@pytest.mark.parametrize("i", range(12))
 def test_long_reestimate_lists_equal_oracle(i, oracle_mod):
     _sweep_case(_long_list_case(i), oracle_mod, min_reestimated=33)
 
