@@ -513,7 +513,14 @@ __device__ bool iterate(const Params& P, const TraceDev& T, Shared& S, const boo
   phase_mark(c, 0);
 #if RS_PREFETCH_HEAD
   if (tid >= kThreads - 32) {  // the last warp: pull the previous head's next candidate rows into L1
-    const int h = S.pf_head, l = tid & 31;
+    int h = S.pf_head;
+    const int l = tid & 31;
+    if constexpr (kPart) {  // large traces: a fully prefilled head is followed by the static order's next entry
+      if (h >= 0 && rq.q[h] >= rq.off[h + 1] - rq.off[h]) {
+        const int z = c.zptr + (rq.zl[c.zptr < T.nzl ? c.zptr : 0] == h ? 1 : 0);
+        h = z < T.nzl ? rq.zl[z] : -1;
+      }
+    }
     if (h >= 0 && l < 18) {
       const int lo = rq.off[h] + rq.q[h], hi = rq.off[h + 1];
       const int r = lo + (l % 9) * 32;  // 9 lines of 128 B cover the <= 256 rows of a candidate
